@@ -1,0 +1,349 @@
+"""Benchmark of the ProxASAGA hot path on B200 (BASELINE.json metric:
+sample updates/s; time-to-1e-6 suboptimality; achieved HBM GB/s vs roofline).
+
+Workload (BASELINE.json configs[1]): l1-logistic,
+n=1e5 x p=5e4, 20 nnz/row Zipf(1.1) columns, fp32 values / int32 indices,
+lambda1 = lambda2 = 1/n, gamma = 1/(2L).  One STEP = one full 30-epoch
+ProxASAGA solve from x0 = 0 (3e6 sample updates): state reset + one
+persistent kernel, inputs resident in HBM.  L2 is flushed (256 MiB write)
+between timed steps, outside the per-step CUDA-event windows.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one process per GPU): config 2 does not shard (SURVEY.md
+§8e) -> N independent replicas (seed = rank), weak scaling; value = updates
+of all ranks / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sample updates/s (ProxASAGA, 30-epoch solve, BASELINE config 2)"
+UNIT = "updates/s"
+FSTAR_FILE = ROOT / "tests" / "golden" / "cfg2_fstar.json"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def workload(rank=0):
+    from paper_1707_06468_b200 import problems
+
+    return problems.config2(seed=rank)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.lines, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(cfg, epochs=30):
+    """The oracle's pthread Hogwild port of run_async (asynchronous.py:131-210)
+    on this host's cores: the full 30-epoch workload (bounded, ~seconds)."""
+    from oracle import oracle as O
+
+    P = O.from_dataset(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"])
+    gamma = 1.0 / (2.0 * P.lipschitz())
+    threads = os.cpu_count() or 1
+    total = epochs * P.n
+    seqs = [O.sample_sequence(0, P.n, c, worker_id=w) for w, c in enumerate(O.split_iterations(total, threads))]
+    t0 = time.perf_counter()
+    x, _, _, cnt = P.run_async(gamma, seqs)
+    dt = time.perf_counter() - t0
+    return {"value": cnt / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"full workload: {epochs} epochs x n={P.n} = {cnt} updates, oracle/sps_oracle.c "
+                      f"oracle_run_async, {threads} pthreads, C11 seq-cst CAS atomics (restates _atomics.c)",
+            "seconds": dt, "objective": P.objective(x)}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (oracle port;
+    the Python reference itself does not exist on the GPU box)."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    cfg = workload(0)
+    P = O.from_dataset(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"])
+    gamma = 1.0 / (2.0 * P.lipschitz())
+    threads = os.cpu_count() or 1
+    per_step = P.n  # one epoch of updates per step (bounded sample of the 30-epoch workload)
+    counts = O.split_iterations(per_step, threads)
+    x = None
+    times = []
+    for s in range(args.warmup + args.steps):
+        seqs = [O.sample_sequence(1000 + s, P.n, c, worker_id=w) for w, c in enumerate(counts)]
+        t0 = time.perf_counter()
+        P.run_async(gamma, seqs)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    tot = float(sum(times))
+    value = args.steps * per_step / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 l1-logistic 1e5x5e4 k=20 zipf1.1; step = 1 epoch (1e5 updates) of the "
+                                   "reference's async algorithm (oracle C port) on host cores"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{per_step} updates per step, {threads} pthreads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
+    """Solve from zero with a device objective checkpoint every epoch; wall =
+    CUDA-event time of kernels + evaluations; log-linear
+    interpolation of the first crossing (asynchronous.py:213-230) on the
+    RELATIVE gap (F - F*)/|F*|."""
+    import torch
+
+    dp.reset_state()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    marks, objs = [], []
+    done = 0
+    evs = []
+    parts = []
+    while done < total:
+        dp.run_async(n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc)
+        done += n
+        pr = dp.objective_parts().clone()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        evs.append(e)
+        parts.append(pr)
+        marks.append(done)
+    torch.cuda.synchronize()
+    walls = [ev0.elapsed_time(e) / 1e3 for e in evs]
+    objs = [float(p.sum().item()) for p in parts]
+    rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
+    hit = None
+    prev_rel, prev_w, prev_it = 1.0, 0.0, 0
+    for it, w, r in zip(marks, walls, rel):
+        if r <= target:
+            import math
+
+            frac = math.log(prev_rel / target) / math.log(prev_rel / r) if prev_rel > r else 1.0
+            hit = (prev_w + frac * (w - prev_w), (prev_it + frac * (it - prev_it)) / n)
+            break
+        prev_rel, prev_w, prev_it = r, w, it
+    return {"target_rel_gap": target, "seconds": hit[0] if hit else None, "epochs": hit[1] if hit else None,
+            "reached": hit is not None, "final_rel_gap": rel[-1], "epochs_run": total / n,
+            "fstar": fstar, "wall_incl_evals_s": walls[-1]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--wpc", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    import paper_1707_06468_b200 as pb
+
+    cfg = workload(rank)
+    data, loss, pen, part = cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"]
+    n = data.n_samples
+    epochs = cfg["epochs"]
+    total = epochs * n
+    dp = pb.DeviceProblem(data, loss, pen, part, drop_dead_blocks=True)
+    gamma = pb.resolve_step_size(cfg["step"], dp.L, n, loss.lambda1)
+    ctas, wpc = args.ctas, args.wpc
+    c_used, w_used, _ = dp.launch_config(dp._sched(1, ctas=ctas, warps_per_cta=wpc))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(s):
+        dp.reset_state()
+        ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ks.record(stream)
+        dp.run_async(total, gamma, seed=1000 * rank + s, ctas=ctas, warps_per_cta=wpc)
+        ke.record(stream)
+        return ks, ke
+
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    steps_ev = []
+    for s in range(args.steps):
+        flush.fill_(s & 0xFF)  # L2 flush between steps (outside the event windows)
+        ss = torch.cuda.Event(enable_timing=True)
+        ss.record(stream)
+        ks, ke = step(args.warmup + s)
+        se = torch.cuda.Event(enable_timing=True)
+        se.record(stream)
+        steps_ev.append((ss, se, ks, ke))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b, _, _ in steps_ev]
+    kern_ms = [c.elapsed_time(d) for _, _, c, d in steps_ev]
+    tot_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([tot_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * args.steps * total / (tot_ms / 1e3)
+    bpu = dp.bytes_per_update()
+    kavg = float(np.mean(kern_ms))
+    achieved = bpu * total / (kavg / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+
+    # ---- time to 1e-6 relative suboptimality (rank 0's problem, seed 0 data)
+    ttt = None
+    if rank == 0 and FSTAR_FILE.exists():
+        fstar = json.loads(FSTAR_FILE.read_text())["fstar"]
+        ttt = time_to_target(dp, gamma, total, n, fstar, seed=7, ctas=ctas, wpc=wpc)
+
+    # ---- end to end through the public API from host buffers
+    e2e_times = []
+    index = pb.build_support_index(data.features, part, drop_dead_blocks=True)  # prebuilt, as a reference user does
+    f = data.features
+    h2d = f.row_offsets.size * 4 + f.col_indices.size * 4 + f.values.size * 4 + data.labels.size * 4
+    d2h = data.n_features * 8 + 2 * 3 * 8
+    for s in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr = pb.run_async(data, loss, pen, part,
+                          pb.AsyncConfig(step_size=cfg["step"], epochs=epochs, seed=500 + s, threads=2,
+                                         checkpoint_every=total), index=index)
+        _ = tr.final_x[0]
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        del tr
+    e2e_val = total / float(np.mean(e2e_times))
+    if dist:
+        t = torch.tensor([e2e_val], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_val = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, epochs)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg2 l1-logistic n={n} p={data.n_features} k=20 zipf1.1 fp32 vals/int32 idx, "
+                                   f"lambda1=lambda2=1/n, gamma=1/(2L); step = full {epochs}-epoch ProxASAGA "
+                                   f"solve from x0=0 ({total} updates)",
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "l2": "256 MiB write between timed steps (outside step events)",
+                       "warps_in_flight": c_used * w_used, "ctas": c_used, "warps_per_cta": w_used,
+                       "bytes_per_update": bpu, "value_storage": "fp32", "state": "fp64 x/abar/D/alpha"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "sps_kernel<float,int,SINGLETON>", "kernel_ms_avg": kavg,
+                         "algorithmic_bytes_per_launch": bpu * total},
+            "time_to_1e-6": ttt,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "api": "paper_1707_06468_b200.run_async(data, loss, penalty, partition, AsyncConfig(epochs=30, "
+                           "threads=2)) from host numpy buffers (upload + ps_prepare + solve + objective + final_x)",
+                    "seconds_per_call": float(np.mean(e2e_times))},
+            "gpu_launches": 2 * args.steps,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * proxsaga.h — C ABI of the B200 (sm_100a) Sparse Proximal SAGA / ProxASAGA
+ * hot path (libproxsaga.so).
+ *
+ * The reference (`sparsesaga`, /root/reference/pkg/src/sparsesaga) runs the
+ * SPS step in Python and exposes one native module, `_atomics`
+ * (_atomics.c:306-335), whose element-level atomics the Python worker loop
+ * calls five times per update (asynchronous.py:92-116).  On B200 the whole
+ * worker loop runs on the device, so the boundary moves up one level: each
+ * entry point below replaces a reference routine (cited per function) and
+ * operates on DEVICE memory owned by the caller (borrowed for the call, like
+ * the Py_buffer views of _atomics.c:16-30).  No torch / CPython types appear.
+ *
+ * Conventions
+ *   - all pointers are device pointers unless stated; `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - return value: PS_OK or an error code; ps_last_error() gives the text.
+ *     The Python layer maps PS_EINVAL -> ValueError, PS_ERANGE -> IndexError,
+ *     PS_ECUDA -> RuntimeError, the conventions of _atomics.c:26,36 and
+ *     saga.py:89-95;
+ *   - coordinate state is one 32-byte record per feature j
+ *       coord[4j+0] = x_j, coord[4j+1] = abar_j, coord[4j+2] = D_j (weight),
+ *       coord[4j+3] = hot-slot tag (reserved)
+ *     so the x / abar / D gather of one coordinate is one 32-byte sector.
+ */
+#ifndef PROXSAGA_H
+#define PROXSAGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_ABI_VERSION 1
+
+enum ps_status { PS_OK = 0, PS_EINVAL = 1, PS_ERANGE = 2, PS_ECUDA = 3, PS_ENOMEM = 4 };
+/* losses.py:15-19 */
+enum ps_loss { PS_LOSS_LOGISTIC = 0, PS_LOSS_SQUARED = 1 };
+/* penalties.py:56-138 */
+enum ps_penalty { PS_PEN_ZERO = 0, PS_PEN_L1 = 1, PS_PEN_GROUP = 2, PS_PEN_BOX = 3 };
+enum ps_dtype { PS_F32 = 0, PS_F64 = 1 };
+enum ps_itype { PS_I32 = 0, PS_I64 = 1 };
+/* data.py:164-191: singleton / contiguous groups (G coords each) / general */
+enum ps_part_kind { PS_PART_SINGLETON = 0, PS_PART_CONTIG = 1, PS_PART_GENERAL = 2 };
+
+/* Row-major CSR, data.py:31-72.  Columns strictly increasing per row. */
+typedef struct ps_csr {
+    int64_t n_rows, n_cols, nnz;
+    const void *row_ptr;     /* n_rows+1, int32 or int64 (row_ptr_type) */
+    const int32_t *col_idx;  /* nnz */
+    const void *values;      /* nnz, fp32 or fp64 (value_type); widened to fp64 before use */
+    const void *labels;      /* n_rows, same type as values */
+    int32_t row_ptr_type;    /* ps_itype */
+    int32_t value_type;      /* ps_dtype */
+} ps_csr_t;
+
+/* Block partition + extended-support index, data.py:121-161, 194-297. */
+typedef struct ps_part {
+    int32_t kind;            /* ps_part_kind */
+    int32_t G;               /* CONTIG: block size (block b = [bG, min(bG+G,p)) ) */
+    int64_t n_blocks;
+    /* GENERAL only (host-provided partition description): */
+    const int32_t *block_of; /* p */
+    const int32_t *blk_ptr;  /* n_blocks+1 */
+    const int32_t *blk_coords; /* p, sorted within each block */
+    /* filled by ps_prepare (device, caller-allocated): */
+    int32_t *blk_count;      /* n_blocks: n_B */
+    double *blk_weight;      /* n_blocks: d_B = n/n_B, 0 if dead */
+    int32_t *row_blk;        /* GENERAL: nnz slots, row i's sorted T_i at row_ptr[i].. */
+    int32_t *row_g;          /* GENERAL: |T_i| */
+    int32_t *spos;           /* GENERAL: nnz, ext slot of each nonzero */
+    int32_t max_slots;       /* set by ps_prepare: max ext slots over rows */
+} ps_part_t;
+
+typedef struct ps_params {
+    int32_t loss;            /* ps_loss */
+    int32_t penalty;         /* ps_penalty */
+    double lambda1;          /* Loss.lambda1 (losses.py:22-31) */
+    double lam2;             /* L1Penalty / GroupL2Penalty weight */
+    double lo, hi;           /* BoxPenalty */
+    double gamma;            /* resolved step (saga.py:25-42) */
+} ps_params_t;
+
+/* Problem statistics written by ps_prepare (host struct). */
+typedef struct ps_stats {
+    int64_t max_count;       /* max_B n_B  (delta = max_count / n, data.py:262) */
+    int64_t n_dead;          /* blocks with n_B = 0 (DeadBlockError, data.py:255-257) */
+    double max_row_sqnorm;   /* max_i ||a_i||^2 (losses.py:99-105) */
+    int32_t max_row_nnz;
+    int32_t max_slots;
+} ps_stats_t;
+
+/* Sample schedule of one ps_run call. */
+typedef struct ps_sched {
+    const int64_t *samples;  /* non-NULL: replay this sequence (deterministic, saga.py:233-256) */
+    int64_t count;           /* updates to perform */
+    uint64_t seed;           /* samples == NULL: on-device counter-based sampler stream */
+    uint64_t slot_base;      /* first slot of the stream used by this call (resume) */
+    unsigned long long *counter; /* device: slots claimed so far (asynchronous.py:68-72) */
+    int32_t batch;           /* slots claimed per counter bump (AsyncConfig.counter_batch) */
+    int32_t ctas;            /* 0 = one wave at full occupancy */
+    int32_t warps_per_cta;   /* 0 = default */
+    int32_t hot_cols;        /* reserved */
+} ps_sched_t;
+
+int ps_abi_version(void);
+const char *ps_last_error(void);
+int ps_device_count(void);
+
+/* data.py:236-297 (build_support_index) + losses.py:99-105: block counts,
+ * weights d_B, delta, dead blocks, max ||a_i||^2, per-row T_i (GENERAL), and
+ * the per-coordinate weight D_j written into coord[4j+2].  Synchronous;
+ * `stats` is host memory. */
+int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, ps_stats_t *stats, void *stream);
+
+/* Scratch bytes ps_run needs in global memory for `warps` resident warps
+ * (0 when every row fits the register path). */
+int64_t ps_scratch_bytes(const ps_csr_t *csr, const ps_part_t *part, int32_t warps);
+
+/* The grid ps_run will launch for this schedule (occupancy-derived when
+ * sched->ctas == 0) and the global scratch it then needs (0 when the
+ * per-warp scratch fits shared memory or is not needed). */
+int ps_launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched,
+                     int32_t *ctas, int32_t *warps_per_cta, int64_t *scratch_bytes);
+
+/* The SPS inner loop.
+ *   sched->samples != NULL: deterministic replay on one warp — saga.py:248-256
+ *     around sps_step (:169-185); fp64 iterates agree with the reference.
+ *   sched->samples == NULL: ProxASAGA, one warp per in-flight sample,
+ *     inconsistent reads, atomicAdd commits on x / abar, atomicExch on alpha_i —
+ *     asynchronous.py:131-210 around worker_iteration (:80-117).
+ * `scratch` may be NULL when ps_scratch_bytes() == 0. */
+int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
+           double *alpha, const ps_sched_t *sched, void *scratch, void *stream);
+
+/* losses.py:134-136 full_objective, computed from x at stride `x_stride`
+ * doubles.  out (device, 3 doubles) = {mean loss, 0.5*lambda1*||x||^2, h(x)}. */
+int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
+                 const double *x, int32_t x_stride, double *out, void *stream);
+
+/* losses.py:118-122 smooth_gradient: grad = A^T l'(Ax)/n + lambda1 x. */
+int ps_smooth_gradient(const ps_csr_t *csr, const ps_params_t *prm, const double *x,
+                       int32_t x_stride, double *grad, void *stream);
+
+/* saga.py:299-317 fixed_point_residual; `grad` is p doubles of workspace;
+ * out (device, 1 double) = ||x - prox_{gamma D phi}(x - gamma D grad f(x))||. */
+int ps_fixed_point_residual(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
+                            const double *coord, double *grad, double *out, void *stream);
+
+/* saga.py:75-78 resync_average: abar = A^T alpha / n, into coord[4j+1]. */
+int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, void *stream);
+
+/* penalties.py:78-81,103-108,134-135,60-61: prox of a vector v[m] with
+ * per-coordinate effective step eff[m] (separable) or eff[0] for the whole
+ * vector as ONE block (group, prox_block). */
+int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
+            void *stream);
+
+/* Solver state to x0 = 0, abar = 0, alpha = 0, counter = 0 (D untouched):
+ * saga.py:231-232. `counter` may be NULL. */
+int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
+                   void *stream);
+
+/* coord record <-> plain vectors: field 0 = x, 1 = abar, 2 = D. */
+int ps_coord_get(const double *coord, int64_t p, int32_t field, double *out, void *stream);
+int ps_coord_set(double *coord, int64_t p, int32_t field, const double *in, void *stream);
+
+/* _atomics.c primitives, device-scope, on caller buffers (test + tooling):
+ *   gather      (_atomics.c:163-209)  out[k] = arr[idx[k]]   (L2-coherent loads)
+ *   scatter_add (_atomics.c:212-258)  arr[idx[k]] += d[k]     (atomicAdd f64)
+ *   exchange    (_atomics.c:260-283)  old[k] = swap(arr[idx[k]], val[k])
+ *   fetch_add_i64 (_atomics.c:285-304)
+ *   add_repeat  (_atomics.c:136-158)  threads x count adds of delta on one cell
+ * Indices are bounds-checked on device: PS_ERANGE if any is outside [0, len). */
+int ps_atomic_gather(const double *arr, int64_t len, const int64_t *idx, int64_t m, double *out,
+                     void *stream);
+int ps_atomic_scatter_add(double *arr, int64_t len, const int64_t *idx, int64_t m, const double *d,
+                          void *stream);
+int ps_atomic_exchange(double *arr, int64_t len, const int64_t *idx, int64_t m, const double *val,
+                       double *old, void *stream);
+int ps_atomic_fetch_add_i64(long long *arr, int64_t len, int64_t i, long long delta, long long *old,
+                            void *stream);
+int ps_atomic_add_repeat(double *cell, double delta, int64_t count, int32_t threads, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

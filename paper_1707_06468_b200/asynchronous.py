@@ -1,0 +1,177 @@
+"""ProxASAGA on the device (mirrors asynchronous.py:1-298).
+
+``run_async`` keeps the reference's signature and trace contract
+(asynchronous.py:131-210).  The reference's Python worker threads become
+resident warps of one persistent kernel (ps_run, async mode): each warp
+claims ``counter_batch`` sample slots at a time from a device counter (the
+reference's batched iteration counter, :156-165), draws its rows from an
+on-device counter-based sampler, reads x / abar inconsistently from L2 and
+commits with atomicAdd / atomicExch.  The monitor (:187-198) becomes a
+host loop that launches one kernel per checkpoint segment and evaluates the
+objective on the device between segments.
+
+``config.threads == 1`` replays worker 0's reference sample stream on a single
+warp, so a 1-thread run equals ``run_sequential`` bit for bit, as in the
+reference (test_async.py:105-112).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .saga import SolverConfig, Trace, _prepare, _problem, _run_meta, worker_rng
+
+
+@dataclass
+class AsyncConfig(SolverConfig):
+    threads: int = 1
+    counter_batch: int = 100
+    warps: int = None           # resident warps (None: full occupancy) when threads > 1
+    warps_per_cta: int = 0      # 0: library default
+
+    def __post_init__(self):
+        super().__post_init__()
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.counter_batch < 1:
+            raise ValueError("counter_batch must be >= 1")
+        if self.warps is not None and self.warps < 1:
+            raise ValueError("warps must be >= 1")
+
+
+def worker_sample_sequence(seed, worker_id, count, n):
+    """asynchronous.py:120-122."""
+    return worker_rng(seed, worker_id).integers(0, n, size=count)
+
+
+def split_iterations(total, threads):
+    """asynchronous.py:125-128."""
+    base = total // threads
+    return [base + (1 if w < total % threads else 0) for w in range(threads)]
+
+
+def _grid(dp, config):
+    if config.warps is None:
+        return 0, config.warps_per_cta
+    wpc = config.warps_per_cta or min(8, config.warps)
+    return max(1, config.warps // wpc), wpc
+
+
+def run_async(data, loss, penalty, partition, config, index=None, track_distance_to=None, max_threads=64,
+              device=None):
+    """Lock-free ProxASAGA (asynchronous.py:131-210) on the device."""
+    if config.threads > max_threads:
+        raise ValueError(f"threads={config.threads} exceeds the cap of {max_threads}")
+    dp = _problem(data, loss, penalty, partition, index, device)
+    n = data.n_samples
+    gamma = _prepare(dp, loss, config, n)
+    every = config.checkpoint_every or n
+    total = config.epochs * n
+    meta = _run_meta(dp, data, loss, penalty, config, gamma, threads=config.threads, algorithm="async-saga")
+    meta["counter_batch"] = config.counter_batch
+    ctas, wpc = _grid(dp, config)
+    if config.threads > 1:
+        c, w, _ = dp.launch_config(dp._sched(1, batch=config.counter_batch, ctas=ctas, warps_per_cta=wpc))
+        meta["warps_in_flight"] = c * w
+    trace = Trace(meta=meta)
+    track = track_distance_to is not None
+    single = config.threads == 1
+    samples = None
+    if single:
+        samples = dp.torch.from_numpy(worker_sample_sequence(config.seed, 0, total, n)).to(dp.device)
+    start = time.perf_counter()
+
+    def checkpoint(it):
+        obj = dp.objective()
+        dist = float(np.sum((dp.x() - track_distance_to) ** 2)) if track else None
+        trace.append(it, n, obj, time.perf_counter() - start, distance=dist, threads=config.threads)
+
+    checkpoint(0)
+    done = 0
+    while done < total:
+        nxt = min(total, done + every)
+        if single:
+            dp.replay(samples[done:nxt], gamma)
+        else:
+            dp.run_async(nxt - done, gamma, seed=config.seed, batch=config.counter_batch, ctas=ctas,
+                         warps_per_cta=wpc)
+        done = nxt
+        checkpoint(done)
+    trace.final_x = dp.x()
+    trace.meta["iterations_run"] = trace.iterations[-1]
+    trace.device_problem = dp
+    trace.shared = dp
+    return trace
+
+
+def iterations_to_target(trace, fstar, target):
+    """Log-linear interpolation of the first crossing (asynchronous.py:213-230)."""
+    floor = 1e-300
+    subopt = [max(o - fstar, floor) for o in trace.objective]
+    for k, s in enumerate(subopt):
+        if s <= target:
+            if k == 0:
+                return trace.iterations[0], trace.wall_seconds[0]
+            s_prev = subopt[k - 1]
+            frac = math.log(s_prev / target) / math.log(s_prev / s)
+            it = trace.iterations[k - 1] + frac * (trace.iterations[k] - trace.iterations[k - 1])
+            wall = trace.wall_seconds[k - 1] + frac * (trace.wall_seconds[k] - trace.wall_seconds[k - 1])
+            return it, wall
+    return None
+
+
+def measure_speedup(data, loss, penalty, partition, config, cores, target_subopt, fstar, device=None):
+    """Iteration and wall speedups to a target (asynchronous.py:233-274).
+
+    On the device "cores" are resident warps: c == 1 replays the reference's
+    single-worker stream; c > 1 runs c warps."""
+    if not cores or cores[0] != 1 or sorted(cores) != list(cores):
+        raise ValueError("cores must be ascending and start with 1")
+    rows, traces, base = [], {}, None
+    for c in cores:
+        run_cfg = AsyncConfig(step_size=config.step_size, epochs=config.epochs, seed=config.seed,
+                              checkpoint_every=config.checkpoint_every, tolerance=0.0,
+                              threads=min(c, 2) if c > 1 else 1, counter_batch=config.counter_batch,
+                              warps=c if c > 1 else None, warps_per_cta=min(8, c) if c > 1 else 0)
+        trace = run_async(data, loss, penalty, partition, run_cfg, device=device)
+        traces[c] = trace
+        hit = iterations_to_target(trace, fstar, target_subopt)
+        if c == 1:
+            base = hit
+        if hit is None or base is None:
+            rows.append({"cores": c, "wall_speedup": float("nan"), "theoretical_speedup": float("nan"),
+                         "reached": False})
+            continue
+        iters, wall = hit
+        base_iters, base_wall = base
+        if c == 1:
+            wall_speedup = theoretical = 1.0
+        else:
+            wall_speedup = base_wall / wall if wall > 0 else float("inf")
+            theoretical = c * base_iters / iters if iters > 0 else float("inf")
+        rows.append({"cores": c, "wall_speedup": wall_speedup, "theoretical_speedup": theoretical,
+                     "reached": True})
+    return rows, traces
+
+
+def speedup_table_csv(rows, path):
+    with open(path, "w") as fh:
+        fh.write("cores,wall_speedup,theoretical_speedup,reached\n")
+        for r in rows:
+            fh.write(f"{r['cores']},{r['wall_speedup']!r},{r['theoretical_speedup']!r},"
+                     f"{str(r['reached']).lower()}\n")
+
+
+def resync_shared_average(trace, data):
+    """Exact abar = A^T alpha / n after the run (asynchronous.py:285-298)."""
+    from .saga import GradientMemory
+
+    dp = trace.device_problem
+    mem = GradientMemory(scalars=dp.alpha.cpu().numpy(), avg=dp.abar())
+    dp.resync_average()
+    mem.avg = dp.abar()
+    return mem

@@ -1,0 +1,734 @@
+// Auxiliary device kernels around the SPS loop:
+//   ps_prepare            K5/K6: block counts n_B, weights d_B, delta, dead
+//                         blocks, max ||a_i||^2, per-row T_i (GENERAL)
+//   ps_objective          K3: full objective (SpMV + loss + ||x||^2 + h(x))
+//   ps_smooth_gradient    K4: A^T l'(Ax)/n + lambda1 x
+//   ps_fixed_point_residual, ps_resync_average, ps_prox, coord get/set,
+//   and the device forms of the reference's _atomics primitives.
+// Reductions are deterministic: per-CTA partials, then one CTA sums them in
+// CTA order.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace ps;
+
+// ---------------------------------------------------------------------------
+// error state
+static thread_local std::string g_err;
+
+int ps_fail(int code, const char *msg)
+{
+    g_err = msg ? msg : "";
+    return code;
+}
+
+int ps_cuda_fail(cudaError_t e, const char *where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return PS_ECUDA;
+}
+
+extern "C" int ps_abi_version(void) { return PS_ABI_VERSION; }
+extern "C" const char *ps_last_error(void) { return g_err.c_str(); }
+extern "C" int ps_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+#define CK(call, where)                                                    \
+    do {                                                                   \
+        cudaError_t _e = (call);                                           \
+        if (_e != cudaSuccess) return ps_cuda_fail(_e, where);             \
+    } while (0)
+
+static int sm_count()
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+template <typename PT> __device__ __forceinline__ int64_t rpx(const void *p, int64_t i)
+{
+    return (int64_t)reinterpret_cast<const PT *>(p)[i];
+}
+template <typename VT> __device__ __forceinline__ double rvx(const void *p, int64_t e)
+{
+    return widen(reinterpret_cast<const VT *>(p)[e]);
+}
+
+// Block-level sum of one double per thread into out[blockIdx.x] (blockDim 256).
+__device__ __forceinline__ void block_sum_store(double v, double *out)
+{
+    __shared__ double red[8];
+    v = warp_sum(v);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double s = l < (int)(blockDim.x >> 5) ? red[l] : 0.0;
+        s = warp_sum(s);
+        if (l == 0) out[blockIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+// Final ordered sum of `nparts` partials (single CTA of 256 threads).
+__global__ void k_finish_sum(const double *parts, int nparts, int ncols, double *out, double scale0)
+{
+    // parts laid out [col][nparts]; out[col] = sum (col 0 scaled by scale0)
+    for (int c = 0; c < ncols; c++) {
+        double v = 0.0;
+        for (int q = threadIdx.x; q < nparts; q += blockDim.x) v += parts[(int64_t)c * nparts + q];
+        __shared__ double red[8];
+        v = warp_sum(v);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
+            out[c] = c == 0 ? s * scale0 : s;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ps_prepare kernels
+
+// per row: ||a_i||^2 (losses.py:99-105 via data.py:74-80), nnz; atomic maxima.
+template <typename VT, typename PT>
+__global__ void k_rowstats(const void *row_ptr, const void *val, int64_t n, unsigned long long *max_sq,
+                           int *max_nnz)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+    double s = 0.0;
+    for (int64_t e = lo; e < hi; e++) {
+        double v = rvx<VT>(val, e);
+        s += v * v;
+    }
+    atomicMax(max_sq, (unsigned long long)__double_as_longlong(s));  // s >= 0: bit order == value order
+    atomicMax(max_nnz, (int)(hi - lo));
+}
+
+// singleton: n_j = #rows containing column j (columns distinct within a row).
+__global__ void k_count_cols(const int32_t *col, int64_t nnz, int32_t *counts)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(counts + col[e], 1);
+}
+
+// contiguous groups: count each distinct block of a row once; max slots.
+template <typename PT>
+__global__ void k_count_contig(const void *row_ptr, const int32_t *col, int64_t n, int G, int32_t *counts,
+                               int *max_slots)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+    int prev = -1, g = 0;
+    for (int64_t e = lo; e < hi; e++) {
+        int b = col[e] / G;
+        if (b != prev) {
+            atomicAdd(counts + b, 1);
+            prev = b;
+            g++;
+        }
+    }
+    atomicMax(max_slots, g * G);
+}
+
+// general partition: per row, sorted unique blocks -> row_blk[lo..lo+g),
+// counts, slot of each nonzero (block offset + rank within the block).
+template <typename PT>
+__global__ void k_index_general(const void *row_ptr, const int32_t *col, int64_t n, const int32_t *block_of,
+                                const int32_t *blk_ptr, const int32_t *blk_coords, int32_t *counts,
+                                int32_t *row_blk, int32_t *row_g, int32_t *spos, int *max_slots)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+    int g = 0;
+    for (int64_t e = lo; e < hi; e++) {  // insertion into a sorted unique list
+        int b = block_of[col[e]];
+        int q = g;
+        while (q > 0 && row_blk[lo + q - 1] > b) q--;
+        if (q > 0 && row_blk[lo + q - 1] == b) continue;
+        for (int r = g; r > q; r--) row_blk[lo + r] = row_blk[lo + r - 1];
+        row_blk[lo + q] = b;
+        g++;
+    }
+    row_g[i] = g;
+    int slots = 0;
+    for (int t = 0; t < g; t++) {
+        int b = row_blk[lo + t];
+        atomicAdd(counts + b, 1);
+        slots += blk_ptr[b + 1] - blk_ptr[b];
+    }
+    atomicMax(max_slots, slots);
+    for (int64_t e = lo; e < hi; e++) {
+        int c = col[e], b = block_of[c];
+        int off = 0, t = 0;
+        while (row_blk[lo + t] != b) {  // blocks sorted: offset = sizes of smaller ones
+            off += blk_ptr[row_blk[lo + t] + 1] - blk_ptr[row_blk[lo + t]];
+            t++;
+        }
+        int a0 = blk_ptr[b], a1 = blk_ptr[b + 1];  // rank of c inside its block
+        while (a0 < a1) {
+            int mid = (a0 + a1) >> 1;
+            if (blk_coords[mid] < c) a0 = mid + 1;
+            else a1 = mid;
+        }
+        spos[e] = off + (a0 - blk_ptr[b]);
+    }
+}
+
+// data.py:259-262: d_B = n / n_B (0 for dead), max n_B, dead count.
+__global__ void k_weights(const int32_t *counts, int64_t nb, int64_t n, double *w, unsigned long long *maxc,
+                          unsigned long long *dead)
+{
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int c = counts[b];
+        w[b] = c > 0 ? (double)n / (double)c : 0.0;
+        if (c == 0) atomicAdd(dead, 1ull);
+        atomicMax(maxc, (unsigned long long)c);
+    }
+}
+
+// coord_weights (data.py:228-233): D_j = d_{B(j)} into coord[4j+2].
+__global__ void k_coord_weights(double *coord, int64_t p, int kind, int G, const int32_t *block_of,
+                                const double *w)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = kind == PS_PART_SINGLETON ? j : (kind == PS_PART_CONTIG ? j / G : block_of[j]);
+        coord[4 * j + 2] = w[b];
+    }
+}
+
+extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, ps_stats_t *stats, void *stream)
+{
+    if (!csr || !part || !coord || !stats) return ps_fail(PS_EINVAL, "null argument");
+    if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
+    if (!part->blk_count || !part->blk_weight) return ps_fail(PS_EINVAL, "blk_count / blk_weight required");
+    if (part->kind == PS_PART_CONTIG && part->G < 1) return ps_fail(PS_EINVAL, "G must be >= 1");
+    if (part->kind == PS_PART_GENERAL &&
+        (!part->block_of || !part->blk_ptr || !part->blk_coords || !part->row_blk || !part->row_g || !part->spos))
+        return ps_fail(PS_EINVAL, "general partition needs block_of/blk_ptr/blk_coords/row_blk/row_g/spos");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t n = csr->n_rows, p = csr->n_cols, nb = part->n_blocks;
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+
+    // tmp: [max_sq u64][maxc u64][dead u64][max_nnz i32][max_slots i32]
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, 64, st), "ps_prepare alloc");
+    CK(cudaMemsetAsync(tmp, 0, 64, st), "ps_prepare memset");
+    unsigned long long *max_sq = (unsigned long long *)tmp;
+    unsigned long long *maxc = max_sq + 1, *dead = max_sq + 2;
+    int *max_nnz = (int *)(max_sq + 3), *max_slots = max_nnz + 1;
+    CK(cudaMemsetAsync(part->blk_count, 0, sizeof(int32_t) * nb, st), "ps_prepare memset counts");
+
+    int tb = 256;
+    int rows_grid = (int)((n + tb - 1) / tb);
+    if (f64 && i64) k_rowstats<double, long long><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->values, n, max_sq, max_nnz);
+    else if (f64) k_rowstats<double, int><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->values, n, max_sq, max_nnz);
+    else if (i64) k_rowstats<float, long long><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->values, n, max_sq, max_nnz);
+    else k_rowstats<float, int><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->values, n, max_sq, max_nnz);
+
+    int grid = sm_count() * 8;
+    if (part->kind == PS_PART_SINGLETON) {
+        if (csr->nnz > 0) k_count_cols<<<grid, tb, 0, st>>>(csr->col_idx, csr->nnz, part->blk_count);
+    } else if (part->kind == PS_PART_CONTIG) {
+        if (i64) k_count_contig<long long><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->G, part->blk_count, max_slots);
+        else k_count_contig<int><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->G, part->blk_count, max_slots);
+    } else {
+        if (i64)
+            k_index_general<long long><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->block_of, part->blk_ptr,
+                                                                  part->blk_coords, part->blk_count, part->row_blk,
+                                                                  part->row_g, part->spos, max_slots);
+        else
+            k_index_general<int><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->block_of, part->blk_ptr,
+                                                            part->blk_coords, part->blk_count, part->row_blk,
+                                                            part->row_g, part->spos, max_slots);
+    }
+    k_weights<<<grid, tb, 0, st>>>(part->blk_count, nb, n, part->blk_weight, maxc, dead);
+    k_coord_weights<<<grid, tb, 0, st>>>(coord, p, part->kind, part->G, part->block_of, part->blk_weight);
+    CK(cudaGetLastError(), "ps_prepare launch");
+
+    unsigned long long h[8];
+    CK(cudaMemcpyAsync(h, tmp, 64, cudaMemcpyDeviceToHost, st), "ps_prepare readback");
+    CK(cudaFreeAsync(tmp, st), "ps_prepare free");
+    CK(cudaStreamSynchronize(st), "ps_prepare sync");
+    int *hi32 = (int *)(h + 3);
+    double msq;
+    std::memcpy(&msq, &h[0], 8);
+    stats->max_row_sqnorm = msq;
+    stats->max_count = (int64_t)h[1];
+    stats->n_dead = (int64_t)h[2];
+    stats->max_row_nnz = hi32[0];
+    stats->max_slots = part->kind == PS_PART_SINGLETON ? hi32[0] : hi32[1];
+    part->max_slots = stats->max_slots;
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// objective: warp per row (grid-stride), then p-coordinate terms.
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(256) k_loss_sum(const void *row_ptr, const int32_t *col, const void *val,
+                                                  const void *y, int64_t n, int loss, const double *x, int xs,
+                                                  double *parts)
+{
+    int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double acc = 0.0;
+    for (int64_t i = w; i < n; i += nw) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        double z = 0.0;
+        for (int64_t e = lo + lane; e < hi; e += 32) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+        z = warp_sum(z);
+        if (lane == 0) acc += loss_value(loss, z, rvx<VT>(y, i));
+    }
+    block_sum_store(acc, parts);
+}
+
+// ||x||^2, penalty partial sums (L1 |x|, box violations) per CTA.
+__global__ void __launch_bounds__(256) k_coord_terms(const double *x, int xs, int64_t p, int pen, double lo,
+                                                     double hi, double *parts_xx, double *parts_pen)
+{
+    double xx = 0.0, pv = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        double v = x[j * xs];
+        xx += v * v;
+        if (pen == PS_PEN_L1) pv += fabs(v);
+        else if (pen == PS_PEN_BOX && !(v >= lo && v <= hi)) pv += 1.0;
+    }
+    block_sum_store(xx, parts_xx);
+    block_sum_store(pv, parts_pen);
+}
+
+// group value (penalties.py:97-101): sum_B ||x_B||_2.
+__global__ void __launch_bounds__(256) k_group_value(const double *x, int xs, int64_t p, int kind, int G,
+                                                     int64_t nb, const int32_t *blk_ptr, const int32_t *blk_coords,
+                                                     double *parts)
+{
+    double acc = 0.0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        double ss = 0.0;
+        if (kind == PS_PART_GENERAL) {
+            for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; q++) {
+                double v = x[(int64_t)blk_coords[q] * xs];
+                ss += v * v;
+            }
+        } else {
+            int64_t g = kind == PS_PART_SINGLETON ? 1 : G;
+            for (int64_t j = b * g; j < min((b + 1) * g, p); j++) {
+                double v = x[j * xs];
+                ss += v * v;
+            }
+        }
+        acc += sqrt(ss);
+    }
+    block_sum_store(acc, parts);
+}
+
+__global__ void k_objective_combine(const double *sums, double lambda1, int pen, double lam2, double *out)
+{
+    // sums: [loss_sum/n, xx, penraw]
+    out[0] = sums[0];
+    out[1] = 0.5 * lambda1 * sums[1];
+    if (pen == PS_PEN_L1 || pen == PS_PEN_GROUP) out[2] = lam2 * sums[2];
+    else if (pen == PS_PEN_BOX) out[2] = sums[2] > 0 ? INFINITY : 0.0;
+    else out[2] = 0.0;
+}
+
+extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
+                            int32_t x_stride, double *out, void *stream)
+{
+    if (!csr || !part || !prm || !x || !out) return ps_fail(PS_EINVAL, "null argument");
+    if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int G1 = std::max(1, sm_count() * 4);  // CTAs per partial pass (fixed -> deterministic)
+    double *parts = nullptr;
+    CK(cudaMallocAsync((void **)&parts, sizeof(double) * (3 * G1 + 3), st), "ps_objective alloc");
+    double *sums = parts + 3 * G1;
+    int64_t n = csr->n_rows, p = csr->n_cols;
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) k_loss_sum<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    else if (f64) k_loss_sum<double, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    else if (i64) k_loss_sum<float, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    else k_loss_sum<float, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    k_coord_terms<<<G1, 256, 0, st>>>(x, x_stride, p, prm->penalty, prm->lo, prm->hi, parts + G1, parts + 2 * G1);
+    if (prm->penalty == PS_PEN_GROUP) {
+        int64_t nb = part->kind == PS_PART_SINGLETON ? p : part->n_blocks;
+        k_group_value<<<G1, 256, 0, st>>>(x, x_stride, p, part->kind, part->G, nb, part->blk_ptr, part->blk_coords,
+                                          parts + 2 * G1);
+    }
+    k_finish_sum<<<1, 256, 0, st>>>(parts, G1, 3, sums, 1.0 / (double)n);
+    k_objective_combine<<<1, 1, 0, st>>>(sums, prm->lambda1, prm->penalty, prm->lam2, out);
+    CK(cudaGetLastError(), "ps_objective launch");
+    CK(cudaFreeAsync(parts, st), "ps_objective free");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// smooth gradient / resync: A^T s via atomic scatter (warp per row).
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(256) k_rmatvec_deriv(const void *row_ptr, const int32_t *col, const void *val,
+                                                       const void *y, int64_t n, int loss, const double *x, int xs,
+                                                       const double *s, double *out, int os)
+{
+    int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < n; i += nw) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        double d;
+        if (s) {
+            d = s[i];
+        } else {
+            double z = 0.0;
+            for (int64_t e = lo + lane; e < hi; e += 32) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+            z = warp_sum(z);
+            d = loss_deriv(loss, z, rvx<VT>(y, i));
+        }
+        for (int64_t e = lo + lane; e < hi; e += 32) atomicAdd(out + (int64_t)col[e] * os, d * rvx<VT>(val, e));
+    }
+}
+
+__global__ void k_fill(double *out, int os, int64_t p, double v)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        out[j * os] = v;
+}
+
+// out = out / n + lambda1 * x   (losses.py:122)
+__global__ void k_grad_finish(double *out, int os, const double *x, int xs, int64_t p, double n, double lambda1)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        double g = out[j * os] / n;
+        out[j * os] = x ? g + lambda1 * x[j * xs] : g;
+    }
+}
+
+static int rmatvec(const ps_csr_t *csr, int loss, const double *x, int xs, const double *s, double *out, int os,
+                   cudaStream_t st)
+{
+    int grid = sm_count() * 8;
+    k_fill<<<grid, 256, 0, st>>>(out, os, csr->n_cols, 0.0);
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    int64_t n = csr->n_rows;
+    if (f64 && i64) k_rmatvec_deriv<double, long long><<<grid, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, loss, x, xs, s, out, os);
+    else if (f64) k_rmatvec_deriv<double, int><<<grid, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, loss, x, xs, s, out, os);
+    else if (i64) k_rmatvec_deriv<float, long long><<<grid, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, loss, x, xs, s, out, os);
+    else k_rmatvec_deriv<float, int><<<grid, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, loss, x, xs, s, out, os);
+    CK(cudaGetLastError(), "rmatvec launch");
+    return PS_OK;
+}
+
+extern "C" int ps_smooth_gradient(const ps_csr_t *csr, const ps_params_t *prm, const double *x, int32_t x_stride,
+                                  double *grad, void *stream)
+{
+    if (!csr || !prm || !x || !grad) return ps_fail(PS_EINVAL, "null argument");
+    if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = rmatvec(csr, prm->loss, x, x_stride, nullptr, grad, 1, st);
+    if (r) return r;
+    k_grad_finish<<<sm_count() * 8, 256, 0, st>>>(grad, 1, x, x_stride, csr->n_cols, (double)csr->n_rows, prm->lambda1);
+    CK(cudaGetLastError(), "ps_smooth_gradient launch");
+    return PS_OK;
+}
+
+extern "C" int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, void *stream)
+{
+    if (!csr || !alpha || !coord) return ps_fail(PS_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = rmatvec(csr, 0, nullptr, 0, alpha, coord + 1, 4, st);
+    if (r) return r;
+    k_grad_finish<<<sm_count() * 8, 256, 0, st>>>(coord + 1, 4, nullptr, 0, csr->n_cols, (double)csr->n_rows, 0.0);
+    CK(cudaGetLastError(), "ps_resync_average launch");
+    return PS_OK;
+}
+
+// fixed-point residual (saga.py:299-317)
+__global__ void __launch_bounds__(256) k_fp_sep(const double *coord, const double *grad, int64_t p, int pen,
+                                                double gamma, double lam2, double lo, double hi, double *parts)
+{
+    double acc = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        double x = coord[4 * j], d = coord[4 * j + 2];
+        double inner = x - gamma * d * grad[j];
+        double z = prox_sep(pen, inner, gamma * d, lam2, lo, hi);
+        double r = x - z;
+        acc += r * r;
+    }
+    block_sum_store(acc, parts);
+}
+
+__global__ void __launch_bounds__(256) k_fp_group(const double *coord, const double *grad, int64_t p, int kind,
+                                                  int G, int64_t nb, const int32_t *blk_ptr,
+                                                  const int32_t *blk_coords, const double *bw, double gamma,
+                                                  double lam2, double *parts)
+{
+    double acc = 0.0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int64_t q0, q1;
+        if (kind == PS_PART_GENERAL) {
+            q0 = blk_ptr[b];
+            q1 = blk_ptr[b + 1];
+        } else {
+            int64_t g = kind == PS_PART_SINGLETON ? 1 : G;
+            q0 = b * g;
+            q1 = min((b + 1) * g, p);
+        }
+        double ss = 0.0;
+        for (int64_t q = q0; q < q1; q++) {
+            int64_t j = kind == PS_PART_GENERAL ? blk_coords[q] : q;
+            double u = coord[4 * j] - gamma * coord[4 * j + 2] * grad[j];
+            ss += u * u;
+        }
+        double f = group_factor(sqrt(ss), gamma * bw[b], lam2);
+        for (int64_t q = q0; q < q1; q++) {
+            int64_t j = kind == PS_PART_GENERAL ? blk_coords[q] : q;
+            double x = coord[4 * j];
+            double u = x - gamma * coord[4 * j + 2] * grad[j];
+            double r = x - u * f;
+            acc += r * r;
+        }
+    }
+    block_sum_store(acc, parts);
+}
+
+__global__ void k_sqrt(double *v) { v[0] = sqrt(v[0]); }
+
+extern "C" int ps_fixed_point_residual(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
+                                       const double *coord, double *grad, double *out, void *stream)
+{
+    if (!csr || !part || !prm || !coord || !grad || !out) return ps_fail(PS_EINVAL, "null argument");
+    if (!(prm->gamma > 0)) return ps_fail(PS_EINVAL, "gamma must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = ps_smooth_gradient(csr, prm, coord, 4, grad, stream);
+    if (r) return r;
+    const int G1 = std::max(1, sm_count() * 4);
+    double *parts = nullptr;
+    CK(cudaMallocAsync((void **)&parts, sizeof(double) * G1, st), "ps_fixed_point_residual alloc");
+    if (prm->penalty == PS_PEN_GROUP) {
+        int64_t nb = part->kind == PS_PART_SINGLETON ? csr->n_cols : part->n_blocks;
+        k_fp_group<<<G1, 256, 0, st>>>(coord, grad, csr->n_cols, part->kind, part->G, nb, part->blk_ptr,
+                                       part->blk_coords, part->blk_weight, prm->gamma, prm->lam2, parts);
+    } else {
+        k_fp_sep<<<G1, 256, 0, st>>>(coord, grad, csr->n_cols, prm->penalty, prm->gamma, prm->lam2, prm->lo, prm->hi,
+                                     parts);
+    }
+    k_finish_sum<<<1, 256, 0, st>>>(parts, G1, 1, out, 1.0);
+    k_sqrt<<<1, 1, 0, st>>>(out);
+    CK(cudaGetLastError(), "ps_fixed_point_residual launch");
+    CK(cudaFreeAsync(parts, st), "ps_fixed_point_residual free");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// standalone prox (penalty API)
+__global__ void k_prox_sep(int pen, const double *v, const double *eff, int64_t m, double lam2, double lo, double hi,
+                           double *out)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = prox_sep(pen, v[q], eff[q], lam2, lo, hi);
+}
+
+__global__ void __launch_bounds__(256) k_prox_group(const double *v, const double *eff, int64_t m, double lam2,
+                                                    double *out)
+{
+    double ss = 0.0;
+    for (int64_t q = threadIdx.x; q < m; q += blockDim.x) ss += v[q] * v[q];
+    __shared__ double red[8];
+    __shared__ double tot;
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
+        tot = s;
+    }
+    __syncthreads();
+    double f = group_factor(sqrt(tot), eff[0], lam2);
+    for (int64_t q = threadIdx.x; q < m; q += blockDim.x) out[q] = v[q] * f;
+}
+
+extern "C" int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
+                       void *stream)
+{
+    if (!prm || !v || !eff || !out) return ps_fail(PS_EINVAL, "null argument");
+    if (m <= 0) return PS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (prm->penalty == PS_PEN_GROUP) k_prox_group<<<1, 256, 0, st>>>(v, eff, m, prm->lam2, out);
+    else k_prox_sep<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(prm->penalty, v, eff, m, prm->lam2,
+                                                                                     prm->lo, prm->hi, out);
+    CK(cudaGetLastError(), "ps_prox launch");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_coord_get(const double *coord, int64_t p, int f, double *out)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = coord[4 * j + f];
+}
+__global__ void k_coord_set(double *coord, int64_t p, int f, const double *in)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        coord[4 * j + f] = in ? in[j] : 0.0;
+}
+
+extern "C" int ps_coord_get(const double *coord, int64_t p, int32_t field, double *out, void *stream)
+{
+    if (!coord || !out || field < 0 || field > 3) return ps_fail(PS_EINVAL, "bad argument");
+    if (p <= 0) return PS_OK;
+    k_coord_get<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(coord, p, field, out);
+    CK(cudaGetLastError(), "ps_coord_get launch");
+    return PS_OK;
+}
+
+extern "C" int ps_coord_set(double *coord, int64_t p, int32_t field, const double *in, void *stream)
+{
+    if (!coord || field < 0 || field > 3) return ps_fail(PS_EINVAL, "bad argument");
+    if (p <= 0) return PS_OK;
+    k_coord_set<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(coord, p, field, in);
+    CK(cudaGetLastError(), "ps_coord_set launch");
+    return PS_OK;
+}
+
+// x0 = 0, abar = 0 (D kept), alpha = 0, counter = 0 in one launch
+// (saga.py:231-232 / PAPER.md:1195-1199).
+__global__ void k_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter)
+{
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t j = t0; j < p; j += stride) {
+        double2 z = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2 *>(coord + 4 * j) = z;
+    }
+    for (int64_t i = t0; i < n; i += stride) alpha[i] = 0.0;
+    if (t0 == 0 && counter) *counter = 0ull;
+}
+
+extern "C" int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
+                              void *stream)
+{
+    if (!coord || !alpha) return ps_fail(PS_EINVAL, "null argument");
+    int64_t m = std::max(p, n);
+    k_state_reset<<<(int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, sm_count() * 8)), 256, 0,
+                    (cudaStream_t)stream>>>(coord, p, alpha, n, counter);
+    CK(cudaGetLastError(), "ps_state_reset launch");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// _atomics primitives
+__global__ void k_check_idx(const int64_t *idx, int64_t m, int64_t len, int *bad)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+        if (idx[q] < 0 || idx[q] >= len) atomicOr(bad, 1);
+}
+__global__ void k_gather(const double *arr, const int64_t *idx, int64_t m, double *out)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = ld_cg(arr + idx[q]);
+}
+__global__ void k_scatter_add(double *arr, const int64_t *idx, int64_t m, const double *d)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(arr + idx[q], d[q]);
+}
+__global__ void k_exchange(double *arr, const int64_t *idx, int64_t m, const double *val, double *old)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+        old[q] = atomic_exch(arr + idx[q], val[q]);
+}
+__global__ void k_fetch_add(long long *arr, int64_t i, long long delta, long long *old)
+{
+    *old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(arr + i), (unsigned long long)delta);
+}
+__global__ void k_add_repeat(double *cell, double delta, int64_t count)
+{
+    for (int64_t k = 0; k < count; k++) atomicAdd(cell, delta);
+}
+
+static int check_indices(const int64_t *idx, int64_t m, int64_t len, cudaStream_t st)
+{
+    if (m <= 0) return PS_OK;
+    int *bad = nullptr, hbad = 0;
+    CK(cudaMallocAsync((void **)&bad, sizeof(int), st), "check alloc");
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), st), "check memset");
+    k_check_idx<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(idx, m, len, bad);
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "check readback");
+    CK(cudaFreeAsync(bad, st), "check free");
+    CK(cudaStreamSynchronize(st), "check sync");
+    if (hbad) return ps_fail(PS_ERANGE, "cell index out of range");
+    return PS_OK;
+}
+
+static inline int grid_for(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 4096)); }
+
+extern "C" int ps_atomic_gather(const double *arr, int64_t len, const int64_t *idx, int64_t m, double *out,
+                                void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = check_indices(idx, m, len, st);
+    if (r) return r;
+    if (m > 0) k_gather<<<grid_for(m), 256, 0, st>>>(arr, idx, m, out);
+    CK(cudaGetLastError(), "ps_atomic_gather");
+    return PS_OK;
+}
+
+extern "C" int ps_atomic_scatter_add(double *arr, int64_t len, const int64_t *idx, int64_t m, const double *d,
+                                     void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = check_indices(idx, m, len, st);
+    if (r) return r;
+    if (m > 0) k_scatter_add<<<grid_for(m), 256, 0, st>>>(arr, idx, m, d);
+    CK(cudaGetLastError(), "ps_atomic_scatter_add");
+    return PS_OK;
+}
+
+extern "C" int ps_atomic_exchange(double *arr, int64_t len, const int64_t *idx, int64_t m, const double *val,
+                                  double *old, void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = check_indices(idx, m, len, st);
+    if (r) return r;
+    if (m > 0) k_exchange<<<grid_for(m), 256, 0, st>>>(arr, idx, m, val, old);
+    CK(cudaGetLastError(), "ps_atomic_exchange");
+    return PS_OK;
+}
+
+extern "C" int ps_atomic_fetch_add_i64(long long *arr, int64_t len, int64_t i, long long delta, long long *old,
+                                       void *stream)
+{
+    if (i < 0 || i >= len) return ps_fail(PS_ERANGE, "cell index out of range");
+    k_fetch_add<<<1, 1, 0, (cudaStream_t)stream>>>(arr, i, delta, old);
+    CK(cudaGetLastError(), "ps_atomic_fetch_add_i64");
+    return PS_OK;
+}
+
+extern "C" int ps_atomic_add_repeat(double *cell, double delta, int64_t count, int32_t threads, void *stream)
+{
+    if (!cell || threads < 1 || count < 0) return ps_fail(PS_EINVAL, "bad argument");
+    int tb = std::min(threads, 256);
+    int grid = (threads + tb - 1) / tb;
+    if (grid * tb != threads) return ps_fail(PS_EINVAL, "threads must be <= 256 or a multiple of 256");
+    k_add_repeat<<<grid, tb, 0, (cudaStream_t)stream>>>(cell, delta, count);
+    CK(cudaGetLastError(), "ps_atomic_add_repeat");
+    return PS_OK;
+}

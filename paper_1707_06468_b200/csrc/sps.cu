@@ -1,0 +1,576 @@
+// The Sparse Proximal SAGA inner loop on sm_100a (ps_run).
+//
+// One warp owns one in-flight sample.  Per update it
+//   1. reads row i of the CSR (coalesced: one nonzero per lane),
+//   2. gathers x^, abar and D on the row's (extended) support -- one 32-byte
+//      coordinate record per coordinate, L2-coherent loads ("inconsistent
+//      read", asynchronous.py:92-96),
+//   3. warp-shuffle dot product -> margin -> loss derivative
+//      (saga.py:161-163, losses.py:73-86),
+//   4. v = D (abar + lambda1 x^) + (new - alpha_i) a_i  (saga.py:164-165),
+//      z = prox_{gamma D}(x^ - gamma v)  (penalties.py:170-186),
+//   5. commits x += z - x^ (atomicAdd, asynchronous.py:104-106),
+//      alpha_i <-> new (atomicExch, :113), abar += ((new-replaced)/n) a_i
+//      (atomicAdd, :114-116).
+// Deterministic mode (sched->samples != NULL) replays a fixed sequence on a
+// single warp with plain stores in the exact order of sps_step
+// (saga.py:169-185): x = x^ + (z - x^), abar += (delta/n) vals, alpha_i = new.
+//
+// Three support layouts (ps_part kind):
+//   SINGLETON  T_i = S_i; rows <= 64 nonzeros stay in registers (fast path),
+//              longer rows go through the per-warp slot scratch.
+//   CONTIG     blocks of G <= 32 contiguous coordinates (config 5); T_i is
+//              derived on the fly from the sorted columns (block = col / G),
+//              blocks are processed G lanes per block with a segmented
+//              shuffle reduction for the group norm.
+//   GENERAL    any BlockPartition; T_i / slot positions precomputed by
+//              ps_prepare; blocks processed one at a time.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ps {
+
+struct KArgs {
+    const void *row_ptr;
+    const int32_t *col;
+    const void *val;
+    const void *y;
+    int64_t n, p;
+    double n_d;
+    // partition
+    int32_t G;
+    const int32_t *blk_ptr, *blk_coords;
+    const int32_t *row_blk, *row_g, *spos;
+    const double *blk_weight;
+    // state
+    double *coord;
+    double *alpha;
+    // params
+    int32_t loss, pen;
+    double lambda1, lam2, lo, hi, gamma;
+    // schedule
+    const int64_t *samples;
+    int64_t count;
+    uint64_t seed, slot_base;
+    unsigned long long *counter;
+    int32_t batch;
+    int32_t det;
+    // scratch
+    double *gscratch;
+    int32_t stride;  // doubles per warp
+    int32_t smem;    // scratch lives in dynamic shared memory
+    int32_t M, GB;   // slot / block capacity per warp
+};
+
+constexpr int NCH = 2;  // register fast path: rows of up to NCH*32 nonzeros
+
+template <typename PT> __device__ __forceinline__ int64_t rp(const void *p, int64_t i)
+{
+    return (int64_t)__ldg(reinterpret_cast<const PT *>(p) + i);
+}
+template <typename VT> __device__ __forceinline__ double rv(const void *p, int64_t e)
+{
+    return widen(__ldg(reinterpret_cast<const VT *>(p) + e));
+}
+
+// alpha_i read (lane 0, broadcast): asynchronous.py:94.
+__device__ __forceinline__ double load_alpha(const KArgs &a, int64_t i, int lane)
+{
+    double old = 0.0;
+    if (lane == 0) old = ld_cg(a.alpha + i);
+    return __shfl_sync(FULL, old, 0);
+}
+
+// alpha_i <- new; returns the value replaced (asynchronous.py:113 / saga.py:185).
+__device__ __forceinline__ double swap_alpha(const KArgs &a, int64_t i, double nw, double old, int lane)
+{
+    double rep = old;
+    if (lane == 0) {
+        if (a.det) a.alpha[i] = nw;
+        else rep = atomic_exch(a.alpha + i, nw);
+    }
+    return __shfl_sync(FULL, rep, 0);
+}
+
+__device__ __forceinline__ void commit_x(const KArgs &a, int64_t c, double xh, double z)
+{
+    if (a.det) a.coord[4 * c] = xh + (z - xh);
+    else red_add(a.coord + 4 * c, z - xh);
+}
+
+__device__ __forceinline__ void commit_abar(const KArgs &a, int64_t c, double inc)
+{
+    if (a.det) {
+        double *p = a.coord + 4 * c + 1;
+        *p = ld_cg(p) + inc;
+    } else {
+        red_add(a.coord + 4 * c + 1, inc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SINGLETON fast path: k <= NCH*32, everything in registers.
+template <typename VT>
+__device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, int k, int lane)
+{
+    int colr[NCH];
+    double vr[NCH], xr[NCH], abr[NCH], dr[NCH];
+    double part = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+        int e = c * 32 + lane;
+        colr[c] = -1;
+        if (e < k) {
+            int col = __ldg(a.col + lo + e);
+            colr[c] = col;
+            vr[c] = rv<VT>(a.val, lo + e);
+            double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
+            xr[c] = xa.x;
+            abr[c] = xa.y;
+            dr[c] = __ldg(a.coord + 4 * (int64_t)col + 2);
+            part += vr[c] * xr[c];
+        }
+    }
+    double old = load_alpha(a, i, lane);
+    double y = rv<VT>(a.y, i);
+    double margin = warp_sum(part);
+    double nw = loss_deriv(a.loss, margin, y);
+    double ds = nw - old;
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+        if (colr[c] >= 0) {
+            double v = dr[c] * (abr[c] + a.lambda1 * xr[c]);
+            v += ds * vr[c];
+            double u = xr[c] - a.gamma * v;
+            double z = prox_sep(a.pen, u, a.gamma * dr[c], a.lam2, a.lo, a.hi);
+            commit_x(a, colr[c], xr[c], z);
+        }
+    }
+    double rep = swap_alpha(a, i, nw, old, lane);
+    double t = (nw - rep) / a.n_d;
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+        if (colr[c] >= 0) {
+            if (a.det) a.coord[4 * (int64_t)colr[c] + 1] = abr[c] + t * vr[c];
+            else red_add(a.coord + 4 * (int64_t)colr[c] + 1, t * vr[c]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Slot path: the extended support is laid out as m "slots" in per-warp
+// scratch (shared or global memory):
+//   sa[s] row value at slot s (0 when the coordinate is not in S_i)
+//   sx[s] x^ at slot s, sv[s] = D (abar^ + lambda1 x^), sw[s] = D
+//   si[s] coordinate id of slot s (-1 = padding), sb[t] block id of rank t,
+//   so[t] first slot of block rank t (GENERAL).
+struct Scratch {
+    double *sa, *sx, *sv, *sw;
+    int *si, *sb, *so;
+};
+
+__device__ __forceinline__ Scratch carve(double *base, int M, int GB)
+{
+    Scratch s;
+    s.sa = base;
+    s.sx = base + M;
+    s.sv = base + 2 * M;
+    s.sw = base + 3 * M;
+    s.si = reinterpret_cast<int *>(base + 4 * M);
+    s.sb = s.si + M;
+    s.so = s.sb + GB;
+    return s;
+}
+
+template <typename VT, int PART>
+__device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane, const Scratch &S)
+{
+    const unsigned lt = (1u << lane) - 1u;
+    int g = 0, m = 0;
+    // ---- 1. blocks of T_i and slot count
+    if (PART == PS_PART_SINGLETON) {
+        m = k;
+    } else if (PART == PS_PART_CONTIG) {
+        int carry = 0, prevblk = -1;
+        for (int base = 0; base < k; base += 32) {
+            int e = base + lane;
+            int blk = e < k ? __ldg(a.col + lo + e) / a.G : -1;
+            int up = __shfl_up_sync(FULL, blk, 1);
+            if (lane == 0) up = prevblk;
+            bool isnew = (e < k) && (blk != up);
+            unsigned bal = __ballot_sync(FULL, isnew);
+            if (isnew) S.sb[carry + __popc(bal & lt)] = blk;
+            carry += __popc(bal);
+            prevblk = __shfl_sync(FULL, blk, 31);
+        }
+        g = carry;
+        m = g * a.G;
+    } else {  // GENERAL
+        g = __ldg(a.row_g + i);
+        int carry = 0;
+        for (int base = 0; base < g; base += 32) {
+            int t = base + lane;
+            int b = 0, sz = 0;
+            if (t < g) {
+                b = __ldg(a.row_blk + lo + t);
+                sz = __ldg(a.blk_ptr + b + 1) - __ldg(a.blk_ptr + b);
+                S.sb[t] = b;
+            }
+            int incl = sz;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (t < g) S.so[t] = carry + incl - sz;
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+        m = carry;
+        if (lane == 0) S.so[g] = m;
+    }
+    __syncwarp();
+    // ---- 2. slot -> coordinate map, zero the row-value slots
+    if (PART == PS_PART_GENERAL) {
+        for (int t = 0; t < g; t++) {
+            int b = S.sb[t], off = S.so[t];
+            int cb = __ldg(a.blk_ptr + b), sz = __ldg(a.blk_ptr + b + 1) - cb;
+            for (int q = lane; q < sz; q += 32) S.si[off + q] = __ldg(a.blk_coords + cb + q);
+        }
+    }
+    for (int s = lane; s < m; s += 32) {
+        S.sa[s] = 0.0;
+        if (PART == PS_PART_SINGLETON) {
+            S.si[s] = __ldg(a.col + lo + s);
+        } else if (PART == PS_PART_CONTIG) {
+            int64_t c = (int64_t)S.sb[s / a.G] * a.G + (s % a.G);
+            S.si[s] = c < a.p ? (int)c : -1;
+        }
+    }
+    __syncwarp();
+    // ---- 3. scatter the row values into their slots
+    if (PART == PS_PART_CONTIG) {
+        int carry = 0, prevblk = -1;
+        for (int base = 0; base < k; base += 32) {
+            int e = base + lane;
+            int col = e < k ? __ldg(a.col + lo + e) : 0;
+            int blk = e < k ? col / a.G : -1;
+            int up = __shfl_up_sync(FULL, blk, 1);
+            if (lane == 0) up = prevblk;
+            bool isnew = (e < k) && (blk != up);
+            unsigned bal = __ballot_sync(FULL, isnew);
+            int rank = carry + __popc(bal & (lt | (1u << lane))) - 1;
+            if (e < k) S.sa[rank * a.G + (col - blk * a.G)] = rv<VT>(a.val, lo + e);
+            carry += __popc(bal);
+            prevblk = __shfl_sync(FULL, blk, 31);
+        }
+    } else {
+        for (int e = lane; e < k; e += 32) {
+            int s = PART == PS_PART_SINGLETON ? e : __ldg(a.spos + lo + e);
+            S.sa[s] = rv<VT>(a.val, lo + e);
+        }
+    }
+    __syncwarp();
+    // ---- 4. gather x^, abar^, D on the extended support; partial margin
+    double part = 0.0;
+    for (int s = lane; s < m; s += 32) {
+        int c = S.si[s];
+        double xh = 0.0, v0 = 0.0, w = 0.0;
+        if (c >= 0) {
+            double2 xa = ld_cg2(a.coord + 4 * (int64_t)c);
+            w = __ldg(a.coord + 4 * (int64_t)c + 2);
+            xh = xa.x;
+            v0 = w * (xa.y + a.lambda1 * xh);
+        }
+        S.sx[s] = xh;
+        S.sv[s] = v0;
+        S.sw[s] = w;
+        part += S.sa[s] * xh;
+    }
+    double old = load_alpha(a, i, lane);
+    double y = rv<VT>(a.y, i);
+    double margin = warp_sum(part);
+    double nw = loss_deriv(a.loss, margin, y);
+    double ds = nw - old;
+    __syncwarp();
+    // ---- 5. prox + commit x on T_i
+    if (a.pen != PS_PEN_GROUP) {
+        for (int s = lane; s < m; s += 32) {
+            int c = S.si[s];
+            if (c < 0) continue;
+            double xh = S.sx[s];
+            double v = S.sv[s] + ds * S.sa[s];
+            double u = xh - a.gamma * v;
+            double z = prox_sep(a.pen, u, a.gamma * S.sw[s], a.lam2, a.lo, a.hi);
+            commit_x(a, c, xh, z);
+        }
+    } else if (PART == PS_PART_CONTIG) {
+        // G lanes per block, bpc blocks per pass; segmented shuffle reduce.
+        const int G = a.G, bpc = 32 / G;
+        const int q = lane % G, tb = lane / G;
+        for (int t0 = 0; t0 < g; t0 += bpc) {
+            int t = t0 + tb;
+            bool on = (tb < bpc) && (t < g);
+            int s = t * G + q;
+            int c = on ? S.si[s] : -1;
+            double xh = 0.0, u = 0.0;
+            if (c >= 0) {
+                xh = S.sx[s];
+                double v = S.sv[s] + ds * S.sa[s];
+                u = xh - a.gamma * v;
+            }
+            double sq = u * u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                double r = __shfl_down_sync(FULL, sq, o);
+                if (q + o < G && lane + o < 32) sq += r;
+            }
+            double ss = __shfl_sync(FULL, sq, lane - q);
+            if (c >= 0) {
+                double eff = a.gamma * a.blk_weight[S.sb[t]];
+                double f = group_factor(sqrt(ss), eff, a.lam2);
+                commit_x(a, c, xh, u * f);
+            }
+        }
+    } else {  // GENERAL group: block at a time
+        for (int t = 0; t < g; t++) {
+            int off = S.so[t], sz = S.so[t + 1] - off;
+            double sq = 0.0;
+            for (int q = lane; q < sz; q += 32) {
+                int s = off + q;
+                double u = S.sx[s] - a.gamma * (S.sv[s] + ds * S.sa[s]);
+                sq += u * u;
+            }
+            double ss = warp_sum(sq);
+            double eff = a.gamma * a.blk_weight[S.sb[t]];
+            double f = group_factor(sqrt(ss), eff, a.lam2);
+            for (int q = lane; q < sz; q += 32) {
+                int s = off + q;
+                double xh = S.sx[s];
+                double u = xh - a.gamma * (S.sv[s] + ds * S.sa[s]);
+                commit_x(a, S.si[s], xh, u * f);
+            }
+        }
+    }
+    // ---- 6. alpha swap, abar on S_i
+    double rep = swap_alpha(a, i, nw, old, lane);
+    double tt = (nw - rep) / a.n_d;
+    for (int e = lane; e < k; e += 32) {
+        int c = __ldg(a.col + lo + e);
+        commit_abar(a, c, tt * rv<VT>(a.val, lo + e));
+    }
+    __syncwarp();
+}
+
+template <typename VT, typename PT, int PART>
+__global__ void __launch_bounds__(256) sps_kernel(const KArgs a)
+{
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    Scratch S{};
+    if (a.stride > 0) {
+        double *base = a.smem ? smem_dyn + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
+        S = carve(base, a.M, a.GB);
+    }
+    uint64_t slot = 0, slot_end = 0;
+    int64_t t = 0;
+    while (true) {
+        int64_t i;
+        if (a.det) {
+            if (t >= a.count) break;
+            i = __ldg(a.samples + t);
+            t++;
+        } else {
+            if (slot >= slot_end) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)a.batch);
+                base = __shfl_sync(FULL, base, 0);
+                if (base >= (unsigned long long)a.count) break;
+                slot = base;
+                slot_end = min((uint64_t)(base + a.batch), (uint64_t)a.count);
+            }
+            i = sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n);
+            slot++;
+        }
+        int64_t lo = rp<PT>(a.row_ptr, i);
+        int k = (int)(rp<PT>(a.row_ptr, i + 1) - lo);
+        if (PART == PS_PART_SINGLETON && k <= NCH * 32) row_reg<VT>(a, i, lo, k, lane);
+        else row_slots<VT, PART>(a, i, lo, k, lane, S);
+        if (a.det) {
+            __threadfence();
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+static int scratch_layout(const ps_csr_t *csr, const ps_part_t *part, int *M, int *GB)
+{
+    // max_slots from ps_prepare; GB bounded by the longest row
+    *M = std::max(1, (int)part->max_slots);
+    *GB = 1;
+    if (part->kind != PS_PART_SINGLETON) *GB = std::max(1, (int)std::min<int64_t>(part->max_slots, csr->n_cols));
+    int ints = *M + 2 * (*GB) + 2;
+    return 4 * (*M) + (ints + 1) / 2;  // doubles per warp
+}
+
+static bool needs_scratch(const ps_csr_t *csr, const ps_part_t *part)
+{
+    if (part->kind != PS_PART_SINGLETON) return true;
+    return part->max_slots > NCH * 32;
+}
+
+extern "C" int64_t ps_scratch_bytes(const ps_csr_t *csr, const ps_part_t *part, int32_t warps)
+{
+    if (!csr || !part || !needs_scratch(csr, part)) return 0;
+    int M, GB;
+    int stride = scratch_layout(csr, part, &M, &GB);
+    return (int64_t)stride * 8 * std::max(warps, 1);
+}
+
+template <typename VT, typename PT, int PART> static void *kernel_ptr()
+{
+    return (void *)sps_kernel<VT, PT, PART>;
+}
+
+static void *pick_kernel(const ps_csr_t *csr, int kind)
+{
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+#define PICK(VT, PT)                                                                 \
+    switch (kind) {                                                                  \
+    case PS_PART_SINGLETON: return kernel_ptr<VT, PT, PS_PART_SINGLETON>();          \
+    case PS_PART_CONTIG: return kernel_ptr<VT, PT, PS_PART_CONTIG>();                \
+    default: return kernel_ptr<VT, PT, PS_PART_GENERAL>();                           \
+    }
+    if (f64 && i64) { PICK(double, long long) }
+    if (f64) { PICK(double, int) }
+    if (i64) { PICK(float, long long) }
+    PICK(float, int)
+#undef PICK
+}
+
+struct LaunchCfg {
+    void *kernel;
+    int ctas, wpc, smem_flag, stride, M, GB;
+    size_t smem;
+    int64_t gscratch_bytes;
+};
+
+static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched, LaunchCfg *L)
+{
+    const bool det = sched->samples != nullptr;
+    L->kernel = pick_kernel(csr, part->kind);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : 8);
+    L->wpc = wpc = std::min(std::max(wpc, 1), 8);
+    L->smem = 0;
+    L->smem_flag = 0;
+    L->stride = L->M = L->GB = 0;
+    L->gscratch_bytes = 0;
+    if (needs_scratch(csr, part)) {
+        L->stride = scratch_layout(csr, part, &L->M, &L->GB);
+        size_t per_cta = (size_t)L->stride * 8 * wpc;
+        if (per_cta <= 96 * 1024) {
+            L->smem_flag = 1;
+            L->smem = per_cta;
+        }
+    }
+    if (L->smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(L->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem);
+        if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run smem attribute");
+    }
+    int per_sm = 1;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->kernel, wpc * 32, L->smem);
+    if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run occupancy");
+    per_sm = std::max(per_sm, 1);
+    L->ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas : sms * per_sm);
+    if (L->stride > 0 && !L->smem_flag) L->gscratch_bytes = (int64_t)L->stride * 8 * wpc * L->ctas;
+    return PS_OK;
+}
+
+extern "C" int ps_launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched, int32_t *ctas,
+                                int32_t *warps_per_cta, int64_t *scratch_bytes)
+{
+    if (!csr || !part || !sched) return ps_fail(PS_EINVAL, "null argument");
+    LaunchCfg L;
+    int r = launch_config(csr, part, sched, &L);
+    if (r) return r;
+    if (ctas) *ctas = L.ctas;
+    if (warps_per_cta) *warps_per_cta = L.wpc;
+    if (scratch_bytes) *scratch_bytes = L.gscratch_bytes;
+    return PS_OK;
+}
+
+extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
+                      double *alpha, const ps_sched_t *sched, void *scratch, void *stream)
+{
+    if (!csr || !part || !prm || !coord || !alpha || !sched) return ps_fail(PS_EINVAL, "null argument");
+    if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
+    if (!(prm->gamma > 0)) return ps_fail(PS_EINVAL, "gamma must be positive");
+    if (part->kind == PS_PART_CONTIG && (part->G < 1 || part->G > 32))
+        return ps_fail(PS_EINVAL, "contiguous partition needs 1 <= G <= 32 (use GENERAL otherwise)");
+    if (prm->penalty == PS_PEN_GROUP && part->kind == PS_PART_SINGLETON)
+        return ps_fail(PS_EINVAL, "group penalty needs a CONTIG (G>=1) or GENERAL partition");
+    if (sched->count < 0) return ps_fail(PS_EINVAL, "negative update count");
+    if (sched->count == 0) return PS_OK;
+    const bool det = sched->samples != nullptr;
+    if (!det && (!sched->counter || sched->batch < 1))
+        return ps_fail(PS_EINVAL, "async mode needs a device counter and batch >= 1");
+
+    KArgs a{};
+    a.row_ptr = csr->row_ptr;
+    a.col = csr->col_idx;
+    a.val = csr->values;
+    a.y = csr->labels;
+    a.n = csr->n_rows;
+    a.p = csr->n_cols;
+    a.n_d = (double)csr->n_rows;
+    a.G = part->G;
+    a.blk_ptr = part->blk_ptr;
+    a.blk_coords = part->blk_coords;
+    a.row_blk = part->row_blk;
+    a.row_g = part->row_g;
+    a.spos = part->spos;
+    a.blk_weight = part->blk_weight;
+    a.coord = coord;
+    a.alpha = alpha;
+    a.loss = prm->loss;
+    a.pen = prm->penalty;
+    a.lambda1 = prm->lambda1;
+    a.lam2 = prm->lam2;
+    a.lo = prm->lo;
+    a.hi = prm->hi;
+    a.gamma = prm->gamma;
+    a.samples = sched->samples;
+    a.count = sched->count;
+    a.seed = sched->seed;
+    a.slot_base = sched->slot_base;
+    a.counter = sched->counter;
+    a.batch = sched->batch;
+    a.det = det ? 1 : 0;
+
+    LaunchCfg L;
+    int r = launch_config(csr, part, sched, &L);
+    if (r) return r;
+    a.stride = L.stride;
+    a.M = L.M;
+    a.GB = L.GB;
+    a.smem = L.smem_flag;
+    if (L.gscratch_bytes > 0) {
+        if (!scratch) return ps_fail(PS_EINVAL, "scratch buffer required (see ps_launch_config)");
+        a.gscratch = (double *)scratch;
+    }
+    void *args[] = {(void *)&a};
+    cudaError_t e = cudaLaunchKernel(L.kernel, dim3(L.ctas), dim3(L.wpc * 32), args, L.smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run launch");
+    return PS_OK;
+}

@@ -1,0 +1,287 @@
+"""Device-resident problem + solver state: the host runtime around libproxsaga.
+
+``DeviceProblem`` uploads a dataset once (CSR with int32 columns, fp32 values
+when that is lossless, int32/int64 row pointers), runs ps_prepare (block
+counts, d_B, delta, max row norm — the reference's build_support_index and
+lipschitz_constant, data.py:236-297 / losses.py:99-105) and owns the
+coordinate state
+
+    coord[p, 4] fp64 = (x_j, abar_j, D_j, reserved)   -- one 32 B sector per j
+    alpha[n]   fp64                                  -- the SAGA scalar memory
+
+(saga.py:54-72 GradientMemory / asynchronous.py:44-72 SharedState).  Every
+computation goes through the C ABI; torch only provides device memory and
+streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .data import partition_structure
+from .penalties import penalty_code
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _f32_exact(a):
+    a = np.asarray(a)
+    if a.dtype == np.float32:
+        return True
+    with np.errstate(over="ignore", invalid="ignore"):
+        return bool(np.array_equal(a.astype(np.float32).astype(np.float64), a))
+
+
+class DeviceProblem:
+    """One problem on one GPU.
+
+    Parameters mirror the reference's solver arguments (saga.py:217-218):
+    ``data`` (Dataset-like: ``features`` CSR with ``row_offsets``,
+    ``col_indices``, ``values``; ``labels``), ``loss`` (``kind``,
+    ``lambda1``), ``penalty`` and ``partition`` (BlockPartition-like, ``None``
+    = singleton).  Reference objects are accepted duck-typed.
+    """
+
+    def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
+                 value_dtype="auto", _labels=None):
+        torch = _torch()
+        _lib.require_device()
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   (device.index if isinstance(device, torch.device) else int(device)))
+        f = data.features if hasattr(data, "features") else data
+        labels = data.labels if _labels is None else _labels
+        self.n, self.p = int(f.n_rows), int(f.n_cols)
+        if self.n < 1:
+            raise ValueError("dataset is empty")
+        if self.p >= 2 ** 31:
+            raise ValueError("n_cols must fit int32")
+        self.nnz = int(f.row_offsets[-1])
+        self.loss_kind = loss.kind if loss is not None else "squared"
+        self.lambda1 = float(loss.lambda1) if loss is not None else 0.0
+        if penalty is None:
+            self.pen_code, self.lam2, self.lo, self.hi = _lib.PEN_ZERO, 0.0, -1.0, 1.0
+        else:
+            self.pen_code, self.lam2, self.lo, self.hi = penalty_code(penalty)
+        dev = self.device
+        with torch.cuda.device(dev):
+            # ---- CSR upload
+            ro = np.asarray(f.row_offsets)
+            self.row_ptr_type = _lib.I32 if self.nnz < 2 ** 31 - 1 else _lib.I64
+            self.row_ptr = torch.from_numpy(np.ascontiguousarray(
+                ro, dtype=np.int32 if self.row_ptr_type == _lib.I32 else np.int64)).to(dev)
+            self.col = torch.from_numpy(np.ascontiguousarray(f.col_indices, dtype=np.int32)).to(dev)
+            vals = np.asarray(f.values)
+            if value_dtype == "auto":
+                use32 = _f32_exact(vals) and _f32_exact(labels)
+            else:
+                use32 = np.dtype(value_dtype) == np.float32
+            self.value_type = _lib.F32 if use32 else _lib.F64
+            vdt = np.float32 if use32 else np.float64
+            self.val = torch.from_numpy(np.ascontiguousarray(vals, dtype=vdt)).to(dev)
+            self.y = torch.from_numpy(np.ascontiguousarray(labels, dtype=vdt)).to(dev)
+            self.csr = _lib.Csr(self.n, self.p, self.nnz, self.row_ptr.data_ptr(), self.col.data_ptr(),
+                                self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
+            # ---- partition
+            self._setup_partition(partition)
+            # ---- state
+            self.coord = torch.zeros((self.p, 4), dtype=torch.float64, device=dev)
+            self.alpha = torch.zeros(self.n, dtype=torch.float64, device=dev)
+            self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.stats = _lib.Stats()
+            _lib.check(_lib.load().ps_prepare(self.csr, self.part, self.coord.data_ptr(), self.stats,
+                                              _lib.stream_ptr()))
+        self.delta = float(self.stats.max_count) / self.n if self.stats.max_count > 0 else 0.0
+        self.n_dead = int(self.stats.n_dead)
+        if self.n_dead and not drop_dead_blocks:
+            from .data import DeadBlockError
+
+            raise DeadBlockError(np.flatnonzero(self.blk_count.cpu().numpy() == 0))
+        self.L = (0.25 if self.loss_kind == "logistic" else 1.0) * float(self.stats.max_row_sqnorm) + self.lambda1
+        self.slot_base = 0
+        self._scratch = None
+        self._out = torch.zeros(4, dtype=torch.float64, device=dev)
+        self._grad = None
+
+    @classmethod
+    def for_index(cls, features, partition, device=None):
+        """Statistics-only instance (no labels needed): build_support_index / L."""
+        class _D:
+            pass
+
+        d = _D()
+        d.features = features
+        return cls(d, None, None, partition, device=device, drop_dead_blocks=True,
+                   _labels=np.zeros(features.n_rows))
+
+    # ------------------------------------------------------------------
+    def _setup_partition(self, partition):
+        torch, dev = self.torch, self.device
+        kind, G = ("singleton", 1) if partition is None else partition_structure(partition)
+        if self.pen_code == _lib.PEN_GROUP and kind == "singleton":
+            kind, G = "contiguous", 1  # per-coordinate blocks through the block path
+        if kind == "contiguous" and G > 32:
+            kind = "general"
+        self.part_kind = kind
+        p = self.p
+        if kind == "singleton":
+            nb = p
+            self.part = _lib.Part(_lib.PART_SINGLETON, 1, nb)
+        elif kind == "contiguous":
+            nb = -(-p // G)
+            self.part = _lib.Part(_lib.PART_CONTIG, G, nb)
+        else:
+            bo = np.asarray(partition.block_of, dtype=np.int64)
+            nb = int(partition.n_blocks)
+            order = np.argsort(bo, kind="stable")
+            ptr = np.zeros(nb + 1, dtype=np.int64)
+            np.cumsum(np.bincount(bo, minlength=nb), out=ptr[1:])
+            self.block_of = torch.from_numpy(bo.astype(np.int32)).to(dev)
+            self.blk_ptr = torch.from_numpy(ptr.astype(np.int32)).to(dev)
+            self.blk_coords = torch.from_numpy(order.astype(np.int32)).to(dev)
+            self.row_blk = torch.zeros(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            self.row_g = torch.zeros(self.n, dtype=torch.int32, device=dev)
+            self.spos = torch.zeros(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            self.part = _lib.Part(_lib.PART_GENERAL, 0, nb, self.block_of.data_ptr(), self.blk_ptr.data_ptr(),
+                                  self.blk_coords.data_ptr(), 0, 0, self.row_blk.data_ptr(),
+                                  self.row_g.data_ptr(), self.spos.data_ptr(), 0)
+        self.n_blocks = nb
+        self.blk_count = torch.zeros(nb, dtype=torch.int32, device=dev)
+        self.blk_weight = torch.zeros(nb, dtype=torch.float64, device=dev)
+        self.part.blk_count = self.blk_count.data_ptr()
+        self.part.blk_weight = self.blk_weight.data_ptr()
+
+    def block_stats(self):
+        return self.blk_count.cpu().numpy(), self.blk_weight.cpu().numpy(), self.stats
+
+    # ------------------------------------------------------------------
+    def params(self, gamma=1.0):
+        return _lib.Params(_lib.LOSS[self.loss_kind], self.pen_code, self.lambda1, self.lam2, self.lo,
+                           self.hi, float(gamma))
+
+    def reset_state(self, stream=None):
+        """x0 = 0, alpha = 0, abar = 0 (PAPER.md:1195-1199 / saga.py:231-232)."""
+        _lib.check(_lib.load().ps_state_reset(self.coord.data_ptr(), self.p, self.alpha.data_ptr(), self.n,
+                                              self.counter.data_ptr(), _lib.stream_ptr(stream)))
+        self.slot_base = 0
+
+    def _sched(self, count, samples=None, seed=0, batch=32, ctas=0, warps_per_cta=0):
+        return _lib.Sched(samples, int(count), int(seed) & (2 ** 64 - 1), int(self.slot_base),
+                          self.counter.data_ptr(), int(batch), int(ctas), int(warps_per_cta), 0)
+
+    def launch_config(self, sched):
+        c, w, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _lib.check(_lib.load().ps_launch_config(self.csr, self.part, sched, ctypes.byref(c), ctypes.byref(w),
+                                                ctypes.byref(b)))
+        return c.value, w.value, b.value
+
+    def _scratch_for(self, sched):
+        _, _, nbytes = self.launch_config(sched)
+        if nbytes == 0:
+            return None
+        if self._scratch is None or self._scratch.numel() * 8 < nbytes:
+            self._scratch = self.torch.empty((nbytes + 7) // 8, dtype=self.torch.float64, device=self.device)
+        return self._scratch.data_ptr()
+
+    def replay(self, samples, gamma, stream=None):
+        """Deterministic replay of a sample sequence (saga.py:248-256) on one warp."""
+        torch = self.torch
+        if isinstance(samples, torch.Tensor) and samples.is_cuda:
+            s = samples.to(torch.int64)
+        else:
+            s = torch.from_numpy(np.ascontiguousarray(samples, dtype=np.int64)).to(self.device)
+        if s.numel() == 0:
+            return
+        if int(s.min()) < 0 or int(s.max()) >= self.n:
+            raise IndexError("sample index out of range")
+        sched = self._sched(s.numel(), samples=s.data_ptr())
+        scr = self._scratch_for(sched)
+        _lib.check(_lib.load().ps_run(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
+                                      self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
+        self._keep = s
+
+    def run_async(self, count, gamma, seed=0, batch=32, ctas=0, warps_per_cta=0, stream=None):
+        """`count` lock-free updates (asynchronous.py:131-210), continuing the
+        sampler stream where the previous call stopped."""
+        self.counter.zero_()
+        sched = self._sched(count, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta)
+        scr = self._scratch_for(sched)
+        _lib.check(_lib.load().ps_run(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
+                                      self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
+        self.slot_base += int(count)
+
+    # ------------------------------------------------------------------
+    def objective_parts(self, x_ptr=None, stride=4, stream=None):
+        """Device tensor [mean loss, l2 term, penalty] (ps_objective)."""
+        if x_ptr is None:
+            x_ptr = self.coord.data_ptr()
+        _lib.check(_lib.load().ps_objective(self.csr, self.part, self.params(), x_ptr, stride,
+                                            self._out.data_ptr(), _lib.stream_ptr(stream)))
+        return self._out[:3]
+
+    def objective(self):
+        v = self.objective_parts().cpu().numpy()
+        return float(v[0] + v[1] + v[2])
+
+    def objective_parts_of(self, x):
+        t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
+        v = self.objective_parts(t.data_ptr(), 1).cpu().numpy()
+        return [float(a) for a in v]
+
+    def objective_of(self, x):
+        a, b, c = self.objective_parts_of(x)
+        return a + b + c
+
+    def smooth_gradient_of(self, x):
+        t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
+        g = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
+        _lib.check(_lib.load().ps_smooth_gradient(self.csr, self.params(), t.data_ptr(), 1, g.data_ptr(),
+                                                  _lib.stream_ptr()))
+        return g.cpu().numpy()
+
+    def fixed_point_residual(self, gamma):
+        """saga.py:299-317 at the current x."""
+        if self._grad is None:
+            self._grad = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
+        _lib.check(_lib.load().ps_fixed_point_residual(self.csr, self.part, self.params(gamma),
+                                                       self.coord.data_ptr(), self._grad.data_ptr(),
+                                                       self._out.data_ptr() + 24, _lib.stream_ptr()))
+        return float(self._out[3].item())
+
+    def resync_average(self):
+        _lib.check(_lib.load().ps_resync_average(self.csr, self.alpha.data_ptr(), self.coord.data_ptr(),
+                                                 _lib.stream_ptr()))
+
+    def field(self, f):
+        out = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
+        _lib.check(_lib.load().ps_coord_get(self.coord.data_ptr(), self.p, f, out.data_ptr(),
+                                            _lib.stream_ptr()))
+        return out
+
+    def x(self):
+        return self.field(0).cpu().numpy()
+
+    def abar(self):
+        return self.field(1).cpu().numpy()
+
+    def weights(self):
+        return self.field(2).cpu().numpy()
+
+    def set_x(self, x):
+        t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
+        _lib.check(_lib.load().ps_coord_set(self.coord.data_ptr(), self.p, 0, t.data_ptr(), _lib.stream_ptr()))
+
+    def bytes_per_update(self, mean_k=None):
+        """Algorithmic bytes per update (SURVEY.md §8d formula, singleton):
+        2 s_ptr + s_y + 2 s_st + k (s_idx + s_val + 5 s_st)."""
+        s_ptr = 4 if self.row_ptr_type == _lib.I32 else 8
+        s_val = 4 if self.value_type == _lib.F32 else 8
+        k = self.nnz / self.n if mean_k is None else mean_k
+        return 2 * s_ptr + s_val + 2 * 8 + k * (4 + s_val + 5 * 8)
