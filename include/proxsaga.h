@@ -101,7 +101,12 @@ typedef struct ps_sched {
     int32_t batch;           /* slots claimed per counter bump (AsyncConfig.counter_batch) */
     int32_t ctas;            /* 0 = one wave at full occupancy */
     int32_t warps_per_cta;   /* 0 = default */
-    int32_t hot_cols;        /* reserved */
+    int32_t hot_cols;        /* H of ps_hot_layout: columns [0,H) staged in shared memory (async) */
+    double contention;       /* c > 0: per-coordinate step gamma_j = gamma * min(1, c * D_j / tau),
+                                tau = effective delay in updates (async only; the fixed point is
+                                unchanged); 0 = plain gamma (the reference's step) */
+    int32_t hot_period;      /* CTA updates between hot flushes (0 = 4 per warp) */
+    int32_t reserved;
 } ps_sched_t;
 
 int ps_abi_version(void);
@@ -157,6 +162,16 @@ int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, v
 int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
             void *stream);
 
+/* Hot-column layout for SINGLETON partitions: columns present in at least
+ * max(ceil(min_frac * n), theta) rows — theta the smallest threshold letting
+ * at most hot_max columns qualify — are renumbered [0, H), the others
+ * [H, p), both in original order; col_inout (the device CSR's column array)
+ * is remapped in place.  perm[old] = new, inv[new] = old (p int32 each);
+ * counts_ws: p int32 workspace.  The SPS kernel stages columns < H in shared
+ * memory (sched->hot_cols = H).  Synchronous; *H_out is host memory. */
+int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
+                  int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out, void *stream);
+
 /* Solver state to x0 = 0, abar = 0, alpha = 0, counter = 0 (D untouched):
  * saga.py:231-232. `counter` may be NULL. */
 int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
@@ -165,6 +180,11 @@ int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned 
 /* coord record <-> plain vectors: field 0 = x, 1 = abar, 2 = D. */
 int ps_coord_get(const double *coord, int64_t p, int32_t field, double *out, void *stream);
 int ps_coord_set(double *coord, int64_t p, int32_t field, const double *in, void *stream);
+/* same through a column permutation: out[j] = coord[4 perm[j] + field] */
+int ps_coord_get_perm(const double *coord, int64_t p, int32_t field, const int32_t *perm, double *out,
+                      void *stream);
+int ps_coord_set_perm(double *coord, int64_t p, int32_t field, const int32_t *perm, const double *in,
+                      void *stream);
 
 /* _atomics.c primitives, device-scope, on caller buffers (test + tooling):
  *   gather      (_atomics.c:163-209)  out[k] = arr[idx[k]]   (L2-coherent loads)

@@ -23,7 +23,8 @@ PART_SINGLETON, PART_CONTIG, PART_GENERAL = 0, 1, 2
 EXPORTS = (
     "ps_abi_version", "ps_last_error", "ps_device_count", "ps_prepare", "ps_scratch_bytes",
     "ps_launch_config", "ps_run", "ps_objective", "ps_smooth_gradient", "ps_fixed_point_residual",
-    "ps_resync_average", "ps_prox", "ps_state_reset", "ps_coord_get", "ps_coord_set", "ps_atomic_gather",
+    "ps_resync_average", "ps_prox", "ps_state_reset", "ps_hot_layout", "ps_coord_get", "ps_coord_set",
+    "ps_coord_get_perm", "ps_coord_set_perm", "ps_atomic_gather",
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat",
 )
@@ -59,7 +60,8 @@ class Stats(ctypes.Structure):
 class Sched(ctypes.Structure):
     _fields_ = [("samples", _vp), ("count", _i64), ("seed", ctypes.c_uint64),
                 ("slot_base", ctypes.c_uint64), ("counter", _vp), ("batch", _i32),
-                ("ctas", _i32), ("warps_per_cta", _i32), ("hot_cols", _i32)]
+                ("ctas", _i32), ("warps_per_cta", _i32), ("hot_cols", _i32), ("contention", _f64),
+                ("hot_period", _i32), ("reserved", _i32)]
 
 
 _P = ctypes.POINTER
@@ -92,6 +94,9 @@ def load():
         "ps_resync_average": (_i32, [_P(Csr), _vp, _vp, _vp]),
         "ps_prox": (_i32, [_P(Params), _vp, _vp, _i64, _vp, _vp]),
         "ps_state_reset": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+        "ps_hot_layout": (_i32, [_P(Csr), _vp, _i32, _f64, _vp, _vp, _vp, _P(_i32), _vp]),
+        "ps_coord_get_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
+        "ps_coord_set_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
         "ps_coord_get": (_i32, [_vp, _i64, _i32, _vp, _vp]),
         "ps_coord_set": (_i32, [_vp, _i64, _i32, _vp, _vp]),
         "ps_atomic_gather": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),

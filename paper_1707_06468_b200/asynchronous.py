@@ -30,8 +30,9 @@ from .saga import SolverConfig, Trace, _prepare, _problem, _run_meta, worker_rng
 class AsyncConfig(SolverConfig):
     threads: int = 1
     counter_batch: int = 100
-    warps: int = None           # resident warps (None: full occupancy) when threads > 1
+    warps: int = None           # resident warps (None: library default grid) when threads > 1
     warps_per_cta: int = 0      # 0: library default
+    contention: float = 2.0     # c of gamma_j = gamma * min(1, c * D_j / warps); 0 = plain gamma
 
     def __post_init__(self):
         super().__post_init__()
@@ -98,7 +99,7 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
             dp.replay(samples[done:nxt], gamma)
         else:
             dp.run_async(nxt - done, gamma, seed=config.seed, batch=config.counter_batch, ctas=ctas,
-                         warps_per_cta=wpc)
+                         warps_per_cta=wpc, contention=config.contention)
         done = nxt
         checkpoint(done)
     trace.final_x = dp.x()

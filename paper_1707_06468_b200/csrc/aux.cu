@@ -8,6 +8,7 @@
 // Reductions are deterministic: per-CTA partials, then one CTA sums them in
 // CTA order.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -630,6 +631,169 @@ extern "C" int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n
     k_state_reset<<<(int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, sm_count() * 8)), 256, 0,
                     (cudaStream_t)stream>>>(coord, p, alpha, n, counter);
     CK(cudaGetLastError(), "ps_state_reset launch");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Hot-column layout (singleton partitions): the columns appearing in at least
+// max(min_frac * n, theta) rows, theta chosen so at most hot_max qualify, are
+// renumbered [0, H) (in original order), the rest [H, p) (in original order),
+// and the CSR column indices are remapped in place.  The SPS kernel then
+// recognises a hot column by `col < H` without any load and stages it in
+// shared memory (SURVEY.md §7.3 "hot-column atomic contention").
+
+__global__ void k_count_ge(const int32_t *counts, int64_t p, int theta, unsigned long long *out)
+{
+    unsigned long long c = 0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        c += counts[j] >= theta;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// chunked exclusive scan of hot flags: pass 1 per-CTA sums
+__global__ void k_flag_sums(const int32_t *counts, int64_t p, int theta, int64_t chunk, int64_t *sums)
+{
+    int64_t lo = blockIdx.x * chunk, hi = min(lo + chunk, p);
+    int64_t c = 0;
+    for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += counts[j] >= theta;
+    __shared__ int64_t red[32];
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_scan_small(int64_t *sums, int nb)
+{
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int b = 0; b < nb; b++) {
+            int64_t v = sums[b];
+            sums[b] = run;
+            run += v;
+        }
+    }
+}
+
+// pass 3: serial-within-CTA rescan (one warp ballot per 32 columns) -> perm
+__global__ void k_perm(const int32_t *counts, int64_t p, int theta, int64_t chunk, const int64_t *offs, int H,
+                       int32_t *perm, int32_t *inv)
+{
+    if (threadIdx.x >= 32) return;
+    int lane = threadIdx.x;
+    int64_t lo = blockIdx.x * chunk, hi = min(lo + chunk, p);
+    int64_t hot_before = offs[blockIdx.x];
+    for (int64_t base = lo; base < hi; base += 32) {
+        int64_t j = base + lane;
+        bool hot = j < hi && counts[j] >= theta;
+        unsigned bal = __ballot_sync(FULL, hot);
+        int64_t r = hot_before + __popc(bal & ((1u << lane) - 1u));
+        if (j < hi) {
+            int64_t nj = hot ? r : H + (j - r);
+            perm[j] = (int32_t)nj;
+            inv[nj] = (int32_t)j;
+        }
+        hot_before += __popc(bal);
+    }
+}
+
+__global__ void k_remap_cols(int32_t *col, int64_t nnz, const int32_t *perm)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+        col[e] = perm[col[e]];
+}
+
+extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
+                             int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out, void *stream)
+{
+    if (!csr || !col_inout || !counts_ws || !perm || !inv || !H_out) return ps_fail(PS_EINVAL, "null argument");
+    if (hot_max < 0) return ps_fail(PS_EINVAL, "hot_max must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t p = csr->n_cols, n = csr->n_rows, nnz = csr->nnz;
+    int grid = sm_count() * 8;
+    CK(cudaMemsetAsync(counts_ws, 0, sizeof(int32_t) * p, st), "ps_hot_layout memset");
+    if (nnz > 0) k_count_cols<<<grid, 256, 0, st>>>(col_inout, nnz, counts_ws);
+    unsigned long long *cnt = nullptr;
+    CK(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long), st), "ps_hot_layout alloc");
+    auto count_ge = [&](int theta, unsigned long long *h) -> int {
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "ps_hot_layout memset");
+        k_count_ge<<<grid, 256, 0, st>>>(counts_ws, p, theta, cnt);
+        CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "ps_hot_layout copy");
+        CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
+        return PS_OK;
+    };
+    // smallest theta >= min_frac*n (and >= 1) with at most hot_max qualifying columns
+    int lo = std::max(1, (int)std::ceil(min_frac * (double)n));
+    unsigned long long h = 0;
+    int r = count_ge(lo, &h);
+    if (r) return r;
+    int theta = lo;
+    if (h > (unsigned long long)hot_max) {
+        int a = lo, b = (int)std::min<int64_t>(n + 1, INT32_MAX);  // count(b) == 0 <= hot_max
+        while (b - a > 1) {
+            int mid = a + (b - a) / 2;
+            r = count_ge(mid, &h);
+            if (r) return r;
+            if (h > (unsigned long long)hot_max) a = mid;
+            else b = mid;
+        }
+        theta = b;
+    }
+    r = count_ge(theta, &h);
+    if (r) return r;
+    int H = (int)h;
+    const int64_t chunk = 1 << 16;
+    int nb = (int)((p + chunk - 1) / chunk);
+    int64_t *sums = nullptr;
+    CK(cudaMallocAsync((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
+    k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, p, theta, chunk, sums);
+    k_scan_small<<<1, 32, 0, st>>>(sums, nb);
+    k_perm<<<nb, 32, 0, st>>>(counts_ws, p, theta, chunk, sums, H, perm, inv);
+    if (nnz > 0) k_remap_cols<<<grid, 256, 0, st>>>(col_inout, nnz, perm);
+    CK(cudaGetLastError(), "ps_hot_layout launch");
+    CK(cudaFreeAsync(sums, st), "ps_hot_layout free");
+    CK(cudaFreeAsync(cnt, st), "ps_hot_layout free");
+    CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
+    *H_out = H;
+    return PS_OK;
+}
+
+// out[j] = coord[4 * perm[j] + f]  (perm: original -> stored index)
+__global__ void k_coord_get_perm(const double *coord, int64_t p, int f, const int32_t *perm, double *out)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = coord[4 * (int64_t)perm[j] + f];
+}
+__global__ void k_coord_set_perm(double *coord, int64_t p, int f, const int32_t *perm, const double *in)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        coord[4 * (int64_t)perm[j] + f] = in[j];
+}
+
+extern "C" int ps_coord_get_perm(const double *coord, int64_t p, int32_t field, const int32_t *perm, double *out,
+                                 void *stream)
+{
+    if (!coord || !out || !perm || field < 0 || field > 3) return ps_fail(PS_EINVAL, "bad argument");
+    if (p <= 0) return PS_OK;
+    k_coord_get_perm<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(coord, p, field,
+                                                                                                  perm, out);
+    CK(cudaGetLastError(), "ps_coord_get_perm launch");
+    return PS_OK;
+}
+
+extern "C" int ps_coord_set_perm(double *coord, int64_t p, int32_t field, const int32_t *perm, const double *in,
+                                 void *stream)
+{
+    if (!coord || !in || !perm || field < 0 || field > 3) return ps_fail(PS_EINVAL, "bad argument");
+    if (p <= 0) return PS_OK;
+    k_coord_set_perm<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(coord, p, field,
+                                                                                                  perm, in);
+    CK(cudaGetLastError(), "ps_coord_set_perm launch");
     return PS_OK;
 }
 

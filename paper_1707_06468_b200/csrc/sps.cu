@@ -51,6 +51,7 @@ struct KArgs {
     // params
     int32_t loss, pen;
     double lambda1, lam2, lo, hi, gamma;
+    double kappa;  // contention scale c / tau (INFINITY: plain gamma)
     // schedule
     const int64_t *samples;
     int64_t count;
@@ -58,6 +59,11 @@ struct KArgs {
     unsigned long long *counter;
     int32_t batch;
     int32_t det;
+    // hot-column staging (SINGLETON, async): columns [0, H) live in shared memory
+    int32_t H;          // 0 = off
+    int32_t period;     // CTA updates between flushes of the pending deltas
+    int32_t hot_doubles;  // shared doubles used by the staging area
+    int32_t hot_own;      // hot reads include this CTA's pending deltas
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -65,7 +71,7 @@ struct KArgs {
     int32_t M, GB;   // slot / block capacity per warp
 };
 
-constexpr int NCH = 2;  // register fast path: rows of up to NCH*32 nonzeros
+constexpr int NCH_MAX = 2;  // register fast path: rows of up to NCH*32 nonzeros (NCH=1 for 1024-thread CTAs)
 
 template <typename PT> __device__ __forceinline__ int64_t rp(const void *p, int64_t i)
 {
@@ -95,6 +101,14 @@ __device__ __forceinline__ double swap_alpha(const KArgs &a, int64_t i, double n
     return __shfl_sync(FULL, rep, 0);
 }
 
+// Per-coordinate step gamma_j = gamma * min(1, kappa * D_j): damps only the
+// coordinates that more than c of the tau in-flight updates touch at once
+// (expected concurrent writers tau / D_j).  kappa = +inf -> exactly gamma.
+__device__ __forceinline__ double step_of(const KArgs &a, double d)
+{
+    return a.gamma * fmin(1.0, a.kappa * d);
+}
+
 __device__ __forceinline__ void commit_x(const KArgs &a, int64_t c, double xh, double z)
 {
     if (a.det) a.coord[4 * c] = xh + (z - xh);
@@ -112,9 +126,81 @@ __device__ __forceinline__ void commit_abar(const KArgs &a, int64_t c, double in
 }
 
 // ---------------------------------------------------------------------------
+// Hot-column staging.  Per CTA, in shared memory:
+//   hx[H], hab[H], hd[H]  snapshot of x, abar, D of the hot columns
+//   pend[NCOPY][2][H]     pending x / abar deltas of this CTA (fp64, smem atomics)
+// Hot reads come from the snapshot (an inconsistent read, like any other);
+// hot commits go to the pending arrays; every `period` CTA updates one warp
+// flushes pending -> global with one RED per (column, field) and refreshes
+// the snapshot.  Cuts same-sector L2 atomics on the Zipf head by ~period x.
+constexpr int NCOPY = 2;
+
+struct HotView {
+    double *x, *ab, *d, *pend;
+    int H;
+};
+
+__device__ __forceinline__ HotView hot_view(double *base, int H)
+{
+    return HotView{base, base + H, base + 2 * H, base + 3 * H, H};
+}
+
+__device__ __forceinline__ double smem_take(double *p)
+{
+    return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
+}
+
+// flush this CTA's pending deltas to global, then refresh the snapshot.
+// Lane l owns slots l, l+32, ... (HOT_PER_LANE of them; the hottest columns
+// spread over lanes); `dirty[l]` has bit k set when slot l+32k has pending
+// deltas.  REDs are fire-and-forget; the refresh loads are issued together so
+// one L2 latency covers all of a lane's slots.
+constexpr int HOT_PER_LANE = 8;  // H <= 256
+constexpr int HOT_MAX = 32 * HOT_PER_LANE;
+
+__device__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
+{
+    unsigned m = atomicExch(dirty + lane, 0u);
+    while (m) {
+        int k = __ffs(m) - 1;
+        m &= m - 1;
+        int s = lane + 32 * k;
+        if (s >= h.H) continue;
+        double dx = 0.0, dab = 0.0;
+#pragma unroll
+        for (int c = 0; c < NCOPY; c++) {
+            dx += smem_take(h.pend + (2 * c) * h.H + s);
+            dab += smem_take(h.pend + (2 * c + 1) * h.H + s);
+        }
+        double *g = a.coord + 4 * (int64_t)s;
+        if (dx != 0.0) red_add(g, dx);
+        if (dab != 0.0) red_add(g + 1, dab);
+    }
+    if (!refresh) return;
+#pragma unroll 1
+    for (int k0 = 0; k0 < HOT_PER_LANE; k0 += 4) {
+        double2 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            int s = lane + 32 * (k0 + k);
+            if (s < h.H) v[k] = ld_cg2(a.coord + 4 * (int64_t)s);  // program order: sees our REDs
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            int s = lane + 32 * (k0 + k);
+            if (s < h.H) {
+                h.x[s] = v[k].x;
+                h.ab[s] = v[k].y;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // SINGLETON fast path: k <= NCH*32, everything in registers.
-template <typename VT>
-__device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, int k, int lane)
+template <typename VT, int NCH>
+__device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, int k, int lane, const HotView &h,
+                                        double *px, double *pab, unsigned *dirty)
 {
     int colr[NCH];
     double vr[NCH], xr[NCH], abr[NCH], dr[NCH];
@@ -127,10 +213,29 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
             int col = __ldg(a.col + lo + e);
             colr[c] = col;
             vr[c] = rv<VT>(a.val, lo + e);
-            double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
-            xr[c] = xa.x;
-            abr[c] = xa.y;
-            dr[c] = __ldg(a.coord + 4 * (int64_t)col + 2);
+            if (col < h.H) {
+                if (a.hot_own & 2) {  // live L2 read of the hot cell (writes still aggregated)
+                    double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
+                    xr[c] = xa.x;
+                    abr[c] = xa.y;
+                } else {
+                    xr[c] = h.x[col];
+                    abr[c] = h.ab[col];
+                }
+                dr[c] = h.d[col];
+                if (a.hot_own & 1) {
+#pragma unroll
+                    for (int q = 0; q < NCOPY; q++) {
+                        xr[c] += h.pend[2 * q * h.H + col];
+                        abr[c] += h.pend[(2 * q + 1) * h.H + col];
+                    }
+                }
+            } else {
+                double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
+                xr[c] = xa.x;
+                abr[c] = xa.y;
+                dr[c] = __ldg(a.coord + 4 * (int64_t)col + 2);
+            }
             part += vr[c] * xr[c];
         }
     }
@@ -144,9 +249,15 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
         if (colr[c] >= 0) {
             double v = dr[c] * (abr[c] + a.lambda1 * xr[c]);
             v += ds * vr[c];
-            double u = xr[c] - a.gamma * v;
-            double z = prox_sep(a.pen, u, a.gamma * dr[c], a.lam2, a.lo, a.hi);
-            commit_x(a, colr[c], xr[c], z);
+            double g = step_of(a, dr[c]);
+            double u = xr[c] - g * v;
+            double z = prox_sep(a.pen, u, g * dr[c], a.lam2, a.lo, a.hi);
+            if (colr[c] < h.H) {
+                atomicAdd(px + colr[c], z - xr[c]);
+                atomicOr(dirty + (colr[c] & 31), 1u << (colr[c] >> 5));
+            } else {
+                commit_x(a, colr[c], xr[c], z);
+            }
         }
     }
     double rep = swap_alpha(a, i, nw, old, lane);
@@ -155,6 +266,10 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
     for (int c = 0; c < NCH; c++) {
         if (colr[c] >= 0) {
             if (a.det) a.coord[4 * (int64_t)colr[c] + 1] = abr[c] + t * vr[c];
+            else if (colr[c] < h.H) {
+                atomicAdd(pab + colr[c], t * vr[c]);
+                atomicOr(dirty + (colr[c] & 31), 1u << (colr[c] >> 5));
+            }
             else red_add(a.coord + 4 * (int64_t)colr[c] + 1, t * vr[c]);
         }
     }
@@ -302,8 +417,9 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             if (c < 0) continue;
             double xh = S.sx[s];
             double v = S.sv[s] + ds * S.sa[s];
-            double u = xh - a.gamma * v;
-            double z = prox_sep(a.pen, u, a.gamma * S.sw[s], a.lam2, a.lo, a.hi);
+            double g = step_of(a, S.sw[s]);
+            double u = xh - g * v;
+            double z = prox_sep(a.pen, u, g * S.sw[s], a.lam2, a.lo, a.hi);
             commit_x(a, c, xh, z);
         }
     } else if (PART == PS_PART_CONTIG) {
@@ -315,11 +431,12 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             bool on = (tb < bpc) && (t < g);
             int s = t * G + q;
             int c = on ? S.si[s] : -1;
-            double xh = 0.0, u = 0.0;
+            double xh = 0.0, u = 0.0, dB = 0.0;
             if (c >= 0) {
+                dB = a.blk_weight[S.sb[t]];
                 xh = S.sx[s];
                 double v = S.sv[s] + ds * S.sa[s];
-                u = xh - a.gamma * v;
+                u = xh - step_of(a, dB) * v;
             }
             double sq = u * u;
 #pragma unroll
@@ -329,7 +446,7 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             }
             double ss = __shfl_sync(FULL, sq, lane - q);
             if (c >= 0) {
-                double eff = a.gamma * a.blk_weight[S.sb[t]];
+                double eff = step_of(a, dB) * dB;
                 double f = group_factor(sqrt(ss), eff, a.lam2);
                 commit_x(a, c, xh, u * f);
             }
@@ -337,19 +454,20 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
     } else {  // GENERAL group: block at a time
         for (int t = 0; t < g; t++) {
             int off = S.so[t], sz = S.so[t + 1] - off;
+            double dB = a.blk_weight[S.sb[t]];
+            double gB = step_of(a, dB);
             double sq = 0.0;
             for (int q = lane; q < sz; q += 32) {
                 int s = off + q;
-                double u = S.sx[s] - a.gamma * (S.sv[s] + ds * S.sa[s]);
+                double u = S.sx[s] - gB * (S.sv[s] + ds * S.sa[s]);
                 sq += u * u;
             }
             double ss = warp_sum(sq);
-            double eff = a.gamma * a.blk_weight[S.sb[t]];
-            double f = group_factor(sqrt(ss), eff, a.lam2);
+            double f = group_factor(sqrt(ss), gB * dB, a.lam2);
             for (int q = lane; q < sz; q += 32) {
                 int s = off + q;
                 double xh = S.sx[s];
-                double u = xh - a.gamma * (S.sv[s] + ds * S.sa[s]);
+                double u = xh - gB * (S.sv[s] + ds * S.sa[s]);
                 commit_x(a, S.si[s], xh, u * f);
             }
         }
@@ -364,17 +482,34 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
     __syncwarp();
 }
 
-template <typename VT, typename PT, int PART>
-__global__ void __launch_bounds__(256) sps_kernel(const KArgs a)
+template <typename VT, typename PT, int PART, int MAXT>
+__global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
 {
     extern __shared__ double smem_dyn[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    // shared layout: [hot staging (hot_doubles) | CTA update counter + dirty[32] (17 doubles) | per-warp scratch]
+    HotView h = hot_view(smem_dyn, a.H);
+    unsigned *upd = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
+    unsigned *dirty = upd + 2;
+    double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
     Scratch S{};
     if (a.stride > 0) {
-        double *base = a.smem ? smem_dyn + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
+        const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
+        double *base = a.smem ? smem_dyn + hdr + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
         S = carve(base, a.M, a.GB);
+    }
+    if (a.H > 0) {
+        for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
+            double2 v = ld_cg2(a.coord + 4 * (int64_t)s);
+            h.x[s] = v.x;
+            h.ab[s] = v.y;
+            h.d[s] = __ldg(a.coord + 4 * (int64_t)s + 2);
+        }
+        for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
+        if (threadIdx.x < 34) upd[threadIdx.x] = 0u;
+        __syncthreads();
     }
     uint64_t slot = 0, slot_end = 0;
     int64_t t = 0;
@@ -398,11 +533,26 @@ __global__ void __launch_bounds__(256) sps_kernel(const KArgs a)
         }
         int64_t lo = rp<PT>(a.row_ptr, i);
         int k = (int)(rp<PT>(a.row_ptr, i + 1) - lo);
-        if (PART == PS_PART_SINGLETON && k <= NCH * 32) row_reg<VT>(a, i, lo, k, lane);
+        constexpr int NCH = MAXT > 256 ? 1 : NCH_MAX;
+        if (PART == PS_PART_SINGLETON && k <= NCH * 32) row_reg<VT, NCH>(a, i, lo, k, lane, h, px, pab, dirty);
         else row_slots<VT, PART>(a, i, lo, k, lane, S);
         if (a.det) {
             __threadfence();
             __syncwarp();
+        }
+        if (a.H > 0) {
+            unsigned old = 0;
+            if (lane == 0) old = atomicAdd(upd, 1u);
+            old = __shfl_sync(FULL, old, 0);
+            if ((old + 1) % (unsigned)a.period == 0) hot_flush(a, h, dirty, lane, true);
+        }
+    }
+    if (a.H > 0) {  // every warp of the CTA has left the loop: final flush
+        __syncthreads();
+        if (wib == 0) {
+            dirty[lane] = 0xffffffffu >> (32 - HOT_PER_LANE);  // flush every slot
+            __syncwarp();
+            hot_flush(a, h, dirty, lane, false);
         }
     }
 }
@@ -421,10 +571,10 @@ static int scratch_layout(const ps_csr_t *csr, const ps_part_t *part, int *M, in
     return 4 * (*M) + (ints + 1) / 2;  // doubles per warp
 }
 
-static bool needs_scratch(const ps_csr_t *csr, const ps_part_t *part)
+static bool needs_scratch(const ps_csr_t *csr, const ps_part_t *part, bool big = false)
 {
     if (part->kind != PS_PART_SINGLETON) return true;
-    return part->max_slots > NCH * 32;
+    return part->max_slots > (big ? 1 : NCH_MAX) * 32;
 }
 
 extern "C" int64_t ps_scratch_bytes(const ps_csr_t *csr, const ps_part_t *part, int32_t warps)
@@ -437,12 +587,22 @@ extern "C" int64_t ps_scratch_bytes(const ps_csr_t *csr, const ps_part_t *part, 
 
 template <typename VT, typename PT, int PART> static void *kernel_ptr()
 {
-    return (void *)sps_kernel<VT, PT, PART>;
+    return (void *)sps_kernel<VT, PT, PART, 256>;
+}
+template <typename VT, typename PT> static void *kernel_ptr_big()
+{
+    return (void *)sps_kernel<VT, PT, PS_PART_SINGLETON, 1024>;
 }
 
-static void *pick_kernel(const ps_csr_t *csr, int kind)
+static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 {
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (big) {
+        if (f64 && i64) return kernel_ptr_big<double, long long>();
+        if (f64) return kernel_ptr_big<double, int>();
+        if (i64) return kernel_ptr_big<float, long long>();
+        return kernel_ptr_big<float, int>();
+    }
 #define PICK(VT, PT)                                                                 \
     switch (kind) {                                                                  \
     case PS_PART_SINGLETON: return kernel_ptr<VT, PT, PS_PART_SINGLETON>();          \
@@ -458,7 +618,7 @@ static void *pick_kernel(const ps_csr_t *csr, int kind)
 
 struct LaunchCfg {
     void *kernel;
-    int ctas, wpc, smem_flag, stride, M, GB;
+    int ctas, wpc, smem_flag, stride, M, GB, H, hot_doubles;
     size_t smem;
     int64_t gscratch_bytes;
 };
@@ -466,22 +626,25 @@ struct LaunchCfg {
 static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched, LaunchCfg *L)
 {
     const bool det = sched->samples != nullptr;
-    L->kernel = pick_kernel(csr, part->kind);
+    L->H = (!det && part->kind == PS_PART_SINGLETON) ? std::min(HOT_MAX, std::max(0, (int)sched->hot_cols)) : 0;
+    L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : 8);
-    L->wpc = wpc = std::min(std::max(wpc, 1), 8);
-    L->smem = 0;
+    bool big = part->kind == PS_PART_SINGLETON && wpc > 8;
+    L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
+    L->kernel = pick_kernel(csr, part->kind, big);
+    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
     L->smem_flag = 0;
     L->stride = L->M = L->GB = 0;
     L->gscratch_bytes = 0;
-    if (needs_scratch(csr, part)) {
+    if (needs_scratch(csr, part, big)) {
         L->stride = scratch_layout(csr, part, &L->M, &L->GB);
         size_t per_cta = (size_t)L->stride * 8 * wpc;
-        if (per_cta <= 96 * 1024) {
+        if (per_cta + L->smem <= 96 * 1024) {
             L->smem_flag = 1;
-            L->smem = per_cta;
+            L->smem += per_cta;
         }
     }
     if (L->smem > 48 * 1024) {
@@ -492,7 +655,10 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->kernel, wpc * 32, L->smem);
     if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run occupancy");
     per_sm = std::max(per_sm, 1);
-    L->ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas : sms * per_sm);
+    // default grid: one full wave, but no more than n/16 warps in flight so a
+    // sample is rarely processed twice concurrently on small problems
+    int64_t cap = std::max<int64_t>(1, csr->n_rows / (16 * (int64_t)wpc));
+    L->ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas : (int)std::min<int64_t>((int64_t)sms * per_sm, cap));
     if (L->stride > 0 && !L->smem_flag) L->gscratch_bytes = (int64_t)L->stride * 8 * wpc * L->ctas;
     return PS_OK;
 }
@@ -561,6 +727,14 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     LaunchCfg L;
     int r = launch_config(csr, part, sched, &L);
     if (r) return r;
+    a.H = L.H;
+    a.hot_doubles = L.hot_doubles;
+    a.hot_own = sched->reserved & 3;
+    a.period = sched->hot_period > 0 ? sched->hot_period : std::max(1, L.wpc / 2);
+    // effective delay: in-flight warps + the staleness of the hot snapshot
+    // (up to period * ctas updates between a CTA's refreshes)
+    double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);
+    a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
     a.stride = L.stride;
     a.M = L.M;
     a.GB = L.GB;

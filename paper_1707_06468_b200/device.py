@@ -50,7 +50,7 @@ class DeviceProblem:
     """
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
-                 value_dtype="auto", _labels=None):
+                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, _labels=None):
         torch = _torch()
         _lib.require_device()
         self.torch = torch
@@ -89,8 +89,11 @@ class DeviceProblem:
             self.y = torch.from_numpy(np.ascontiguousarray(labels, dtype=vdt)).to(dev)
             self.csr = _lib.Csr(self.n, self.p, self.nnz, self.row_ptr.data_ptr(), self.col.data_ptr(),
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
-            # ---- partition
+            # ---- partition (+ hot-column renumbering for singleton layouts)
             self._setup_partition(partition)
+            self.H, self.perm, self.perm_np = 0, None, None
+            if self.part_kind == "singleton" and hot_max > 0 and self.n >= 4096:
+                self._hot_layout(int(hot_max), float(hot_min_frac))
             # ---- state
             self.coord = torch.zeros((self.p, 4), dtype=torch.float64, device=dev)
             self.alpha = torch.zeros(self.n, dtype=torch.float64, device=dev)
@@ -103,7 +106,7 @@ class DeviceProblem:
         if self.n_dead and not drop_dead_blocks:
             from .data import DeadBlockError
 
-            raise DeadBlockError(np.flatnonzero(self.blk_count.cpu().numpy() == 0))
+            raise DeadBlockError(np.flatnonzero(self.block_stats()[0] == 0))
         self.L = (0.25 if self.loss_kind == "logistic" else 1.0) * float(self.stats.max_row_sqnorm) + self.lambda1
         self.slot_base = 0
         self._scratch = None
@@ -158,8 +161,36 @@ class DeviceProblem:
         self.part.blk_count = self.blk_count.data_ptr()
         self.part.blk_weight = self.blk_weight.data_ptr()
 
+    def _hot_layout(self, hot_max, min_frac):
+        """ps_hot_layout: the most frequent columns become [0, H) (staged in
+        shared memory by the async kernel); the device CSR is remapped in place."""
+        torch, dev = self.torch, self.device
+        ws = torch.empty(self.p, dtype=torch.int32, device=dev)
+        self.perm = torch.empty(self.p, dtype=torch.int32, device=dev)
+        self.inv = torch.empty(self.p, dtype=torch.int32, device=dev)
+        H = ctypes.c_int32(0)
+        _lib.check(_lib.load().ps_hot_layout(self.csr, self.col.data_ptr(), hot_max, min_frac, ws.data_ptr(),
+                                             self.perm.data_ptr(), self.inv.data_ptr(), ctypes.byref(H),
+                                             _lib.stream_ptr()))
+        self.H = H.value
+        self.perm_np = self.perm.cpu().numpy().astype(np.int64)
+
+    def _to_stored(self, v):
+        """original-order vector -> stored (permuted) order"""
+        if self.perm_np is None:
+            return np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty(self.p)
+        out[self.perm_np] = v
+        return out
+
+    def _to_original(self, v):
+        return v if self.perm_np is None else np.asarray(v)[self.perm_np]
+
     def block_stats(self):
-        return self.blk_count.cpu().numpy(), self.blk_weight.cpu().numpy(), self.stats
+        c, w = self.blk_count.cpu().numpy(), self.blk_weight.cpu().numpy()
+        if self.perm_np is not None:
+            c, w = c[self.perm_np], w[self.perm_np]
+        return c, w, self.stats
 
     # ------------------------------------------------------------------
     def params(self, gamma=1.0):
@@ -172,9 +203,11 @@ class DeviceProblem:
                                               self.counter.data_ptr(), _lib.stream_ptr(stream)))
         self.slot_base = 0
 
-    def _sched(self, count, samples=None, seed=0, batch=32, ctas=0, warps_per_cta=0):
+    def _sched(self, count, samples=None, seed=0, batch=32, ctas=0, warps_per_cta=0, contention=0.0,
+               hot=True, hot_period=0, flags=0):
         return _lib.Sched(samples, int(count), int(seed) & (2 ** 64 - 1), int(self.slot_base),
-                          self.counter.data_ptr(), int(batch), int(ctas), int(warps_per_cta), 0)
+                          self.counter.data_ptr(), int(batch), int(ctas), int(warps_per_cta),
+                          int(self.H if hot else 0), float(contention), int(hot_period), int(flags))
 
     def launch_config(self, sched):
         c, w, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
@@ -207,11 +240,15 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self._keep = s
 
-    def run_async(self, count, gamma, seed=0, batch=32, ctas=0, warps_per_cta=0, stream=None):
+    def run_async(self, count, gamma, seed=0, batch=32, ctas=0, warps_per_cta=0, contention=2.0, hot=True,
+                  hot_period=0, flags=0, stream=None):
         """`count` lock-free updates (asynchronous.py:131-210), continuing the
-        sampler stream where the previous call stopped."""
+        sampler stream where the previous call stopped.  ``contention`` = c of
+        the per-coordinate step gamma_j = gamma min(1, c D_j / tau) (0: plain
+        gamma)."""
         self.counter.zero_()
-        sched = self._sched(count, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta)
+        sched = self._sched(count, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta,
+                            contention=contention, hot=hot, hot_period=hot_period, flags=flags)
         scr = self._scratch_for(sched)
         _lib.check(_lib.load().ps_run(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
@@ -231,7 +268,7 @@ class DeviceProblem:
         return float(v[0] + v[1] + v[2])
 
     def objective_parts_of(self, x):
-        t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
+        t = self.torch.from_numpy(self._to_stored(x)).to(self.device)
         v = self.objective_parts(t.data_ptr(), 1).cpu().numpy()
         return [float(a) for a in v]
 
@@ -240,11 +277,11 @@ class DeviceProblem:
         return a + b + c
 
     def smooth_gradient_of(self, x):
-        t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
+        t = self.torch.from_numpy(self._to_stored(x)).to(self.device)
         g = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
         _lib.check(_lib.load().ps_smooth_gradient(self.csr, self.params(), t.data_ptr(), 1, g.data_ptr(),
                                                   _lib.stream_ptr()))
-        return g.cpu().numpy()
+        return self._to_original(g.cpu().numpy())
 
     def fixed_point_residual(self, gamma):
         """saga.py:299-317 at the current x."""
@@ -260,9 +297,14 @@ class DeviceProblem:
                                                  _lib.stream_ptr()))
 
     def field(self, f):
+        """Field f (0 x, 1 abar, 2 D) of every coordinate, in ORIGINAL column order."""
         out = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
-        _lib.check(_lib.load().ps_coord_get(self.coord.data_ptr(), self.p, f, out.data_ptr(),
-                                            _lib.stream_ptr()))
+        if self.perm is not None:
+            _lib.check(_lib.load().ps_coord_get_perm(self.coord.data_ptr(), self.p, f, self.perm.data_ptr(),
+                                                     out.data_ptr(), _lib.stream_ptr()))
+        else:
+            _lib.check(_lib.load().ps_coord_get(self.coord.data_ptr(), self.p, f, out.data_ptr(),
+                                                _lib.stream_ptr()))
         return out
 
     def x(self):
@@ -276,7 +318,11 @@ class DeviceProblem:
 
     def set_x(self, x):
         t = self.torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.device)
-        _lib.check(_lib.load().ps_coord_set(self.coord.data_ptr(), self.p, 0, t.data_ptr(), _lib.stream_ptr()))
+        if self.perm is not None:
+            _lib.check(_lib.load().ps_coord_set_perm(self.coord.data_ptr(), self.p, 0, self.perm.data_ptr(),
+                                                     t.data_ptr(), _lib.stream_ptr()))
+        else:
+            _lib.check(_lib.load().ps_coord_set(self.coord.data_ptr(), self.p, 0, t.data_ptr(), _lib.stream_ptr()))
 
     def bytes_per_update(self, mean_k=None):
         """Algorithmic bytes per update (SURVEY.md §8d formula, singleton):
