@@ -98,14 +98,19 @@ typedef struct ps_sched {
     uint64_t seed;           /* samples == NULL: on-device counter-based sampler stream */
     uint64_t slot_base;      /* first slot of the stream used by this call (resume) */
     unsigned long long *counter; /* device: slots claimed so far (asynchronous.py:68-72) */
-    int32_t batch;           /* slots claimed per counter bump (AsyncConfig.counter_batch) */
+    int32_t batch;           /* 0: static split of the slots over warps (split_iterations,
+                                asynchronous.py:125-128), counter bumped once per warp;
+                                > 0: warps claim `batch` slots at a time from the counter */
     int32_t ctas;            /* 0 = one wave at full occupancy */
     int32_t warps_per_cta;   /* 0 = default */
     int32_t hot_cols;        /* H of ps_hot_layout: columns [0,H) staged in shared memory (async) */
     double contention;       /* c > 0: per-coordinate step gamma_j = gamma * min(1, c * D_j / tau),
                                 tau = effective delay in updates (async only; the fixed point is
                                 unchanged); 0 = plain gamma (the reference's step) */
-    int32_t hot_period;      /* CTA updates between hot flushes (0 = 4 per warp) */
+    int32_t hot_period;      /* CTA updates between hot flushes (0 = default) */
+    int32_t flags;           /* bit0: hot reads add this CTA's pending deltas; bit1: hot reads
+                                from L2 instead of the snapshot (diagnostics) */
+    int32_t hot_shift;       /* log2 of the hot-record stride of ps_hot_layout */
     int32_t reserved;
 } ps_sched_t;
 
@@ -164,13 +169,17 @@ int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t 
 
 /* Hot-column layout for SINGLETON partitions: columns present in at least
  * max(ceil(min_frac * n), theta) rows — theta the smallest threshold letting
- * at most hot_max columns qualify — are renumbered [0, H), the others
- * [H, p), both in original order; col_inout (the device CSR's column array)
- * is remapped in place.  perm[old] = new, inv[new] = old (p int32 each);
- * counts_ws: p int32 workspace.  The SPS kernel stages columns < H in shared
- * memory (sched->hot_cols = H).  Synchronous; *H_out is host memory. */
+ * at most hot_max columns qualify — are the H hot columns; hot rank r is
+ * stored at index r * S (S = *stride_inout, a power of two, reduced until
+ * S * H <= p) so consecutive hot records sit in different L2 slices; cold
+ * columns fill the remaining indices in original order.  col_inout (the
+ * device CSR's column array) is remapped in place.  perm[old] = new,
+ * inv[new] = old (p int32 each); counts_ws: p int32 workspace.  The SPS
+ * kernel stages hot columns in shared memory (sched->hot_cols = H,
+ * sched->hot_shift = log2 S).  Synchronous; *H_out / *stride_inout host. */
 int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
-                  int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out, void *stream);
+                  int32_t *stride_inout, int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out,
+                  void *stream);
 
 /* Solver state to x0 = 0, abar = 0, alpha = 0, counter = 0 (D untouched):
  * saga.py:231-232. `counter` may be NULL. */

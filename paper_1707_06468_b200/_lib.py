@@ -61,7 +61,7 @@ class Sched(ctypes.Structure):
     _fields_ = [("samples", _vp), ("count", _i64), ("seed", ctypes.c_uint64),
                 ("slot_base", ctypes.c_uint64), ("counter", _vp), ("batch", _i32),
                 ("ctas", _i32), ("warps_per_cta", _i32), ("hot_cols", _i32), ("contention", _f64),
-                ("hot_period", _i32), ("reserved", _i32)]
+                ("hot_period", _i32), ("flags", _i32), ("hot_shift", _i32), ("reserved", _i32)]
 
 
 _P = ctypes.POINTER
@@ -94,7 +94,7 @@ def load():
         "ps_resync_average": (_i32, [_P(Csr), _vp, _vp, _vp]),
         "ps_prox": (_i32, [_P(Params), _vp, _vp, _i64, _vp, _vp]),
         "ps_state_reset": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
-        "ps_hot_layout": (_i32, [_P(Csr), _vp, _i32, _f64, _vp, _vp, _vp, _P(_i32), _vp]),
+        "ps_hot_layout": (_i32, [_P(Csr), _vp, _i32, _f64, _P(_i32), _vp, _vp, _vp, _P(_i32), _vp]),
         "ps_coord_get_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
         "ps_coord_set_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
         "ps_coord_get": (_i32, [_vp, _i64, _i32, _vp, _vp]),

@@ -98,7 +98,7 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
         if single:
             dp.replay(samples[done:nxt], gamma)
         else:
-            dp.run_async(nxt - done, gamma, seed=config.seed, batch=config.counter_batch, ctas=ctas,
+            dp.run_async(nxt - done, gamma, seed=config.seed, batch=0, ctas=ctas,
                          warps_per_cta=wpc, contention=config.contention)
         done = nxt
         checkpoint(done)

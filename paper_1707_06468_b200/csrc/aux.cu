@@ -680,9 +680,18 @@ __global__ void k_scan_small(int64_t *sums, int nb)
     }
 }
 
+// stored index of the c-th cold column when hot ranks r sit at r * S
+__device__ __forceinline__ int64_t cold_pos(int64_t c, int64_t H, int64_t S)
+{
+    if (S == 1) return H + c;
+    int64_t gaps = (S - 1) * H;
+    if (c < gaps) return (c / (S - 1)) * S + 1 + (c % (S - 1));
+    return S * H + (c - gaps);
+}
+
 // pass 3: serial-within-CTA rescan (one warp ballot per 32 columns) -> perm
 __global__ void k_perm(const int32_t *counts, int64_t p, int theta, int64_t chunk, const int64_t *offs, int H,
-                       int32_t *perm, int32_t *inv)
+                       int S, int32_t *perm, int32_t *inv)
 {
     if (threadIdx.x >= 32) return;
     int lane = threadIdx.x;
@@ -694,7 +703,7 @@ __global__ void k_perm(const int32_t *counts, int64_t p, int theta, int64_t chun
         unsigned bal = __ballot_sync(FULL, hot);
         int64_t r = hot_before + __popc(bal & ((1u << lane) - 1u));
         if (j < hi) {
-            int64_t nj = hot ? r : H + (j - r);
+            int64_t nj = hot ? r * S : cold_pos(j - r, H, S);
             perm[j] = (int32_t)nj;
             inv[nj] = (int32_t)j;
         }
@@ -709,9 +718,13 @@ __global__ void k_remap_cols(int32_t *col, int64_t nnz, const int32_t *perm)
 }
 
 extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
-                             int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out, void *stream)
+                             int32_t *stride_inout, int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out,
+                             void *stream)
 {
-    if (!csr || !col_inout || !counts_ws || !perm || !inv || !H_out) return ps_fail(PS_EINVAL, "null argument");
+    if (!csr || !col_inout || !counts_ws || !perm || !inv || !H_out || !stride_inout)
+        return ps_fail(PS_EINVAL, "null argument");
+    if (*stride_inout < 1 || (*stride_inout & (*stride_inout - 1)))
+        return ps_fail(PS_EINVAL, "stride must be a power of two");
     if (hot_max < 0) return ps_fail(PS_EINVAL, "hot_max must be >= 0");
     cudaStream_t st = (cudaStream_t)stream;
     int64_t p = csr->n_cols, n = csr->n_rows, nnz = csr->nnz;
@@ -747,19 +760,22 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t ho
     r = count_ge(theta, &h);
     if (r) return r;
     int H = (int)h;
+    int S = *stride_inout;
+    while (S > 1 && (int64_t)S * H > p) S >>= 1;  // hot records at 0, S, 2S, ...
     const int64_t chunk = 1 << 16;
     int nb = (int)((p + chunk - 1) / chunk);
     int64_t *sums = nullptr;
     CK(cudaMallocAsync((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
     k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, p, theta, chunk, sums);
     k_scan_small<<<1, 32, 0, st>>>(sums, nb);
-    k_perm<<<nb, 32, 0, st>>>(counts_ws, p, theta, chunk, sums, H, perm, inv);
+    k_perm<<<nb, 32, 0, st>>>(counts_ws, p, theta, chunk, sums, H, S, perm, inv);
     if (nnz > 0) k_remap_cols<<<grid, 256, 0, st>>>(col_inout, nnz, perm);
     CK(cudaGetLastError(), "ps_hot_layout launch");
     CK(cudaFreeAsync(sums, st), "ps_hot_layout free");
     CK(cudaFreeAsync(cnt, st), "ps_hot_layout free");
     CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
     *H_out = H;
+    *stride_inout = S;
     return PS_OK;
 }
 

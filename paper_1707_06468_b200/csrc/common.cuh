@@ -106,9 +106,10 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z)
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
-__device__ __forceinline__ int64_t sample_row(uint64_t seed, uint64_t slot, uint64_t n)
+__device__ __forceinline__ int64_t sample_row(uint64_t seed_mix, uint64_t slot, uint64_t n)
 {
-    uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull ^ splitmix64(slot));
+    // seed_mix = splitmix64(seed) precomputed on the host side of the launch
+    uint64_t h = splitmix64(seed_mix + slot * 0x9E3779B97F4A7C15ull);
     return (int64_t)__umul64hi(h, n);
 }
 

@@ -51,7 +51,8 @@ struct KArgs {
     // params
     int32_t loss, pen;
     double lambda1, lam2, lo, hi, gamma;
-    double kappa;  // contention scale c / tau (INFINITY: plain gamma)
+    double kappa;      // contention scale c / tau (INFINITY: plain gamma)
+    double kappa_hot;  // the same for shared-memory-staged hot columns
     // schedule
     const int64_t *samples;
     int64_t count;
@@ -63,7 +64,8 @@ struct KArgs {
     int32_t H;          // 0 = off
     int32_t period;     // CTA updates between flushes of the pending deltas
     int32_t hot_doubles;  // shared doubles used by the staging area
-    int32_t hot_own;      // hot reads include this CTA's pending deltas
+    int32_t hot_shift;    // hot slot r is stored at coordinate r << hot_shift
+    uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -130,9 +132,10 @@ __device__ __forceinline__ void commit_abar(const KArgs &a, int64_t c, double in
 //   hx[H], hab[H], hd[H]  snapshot of x, abar, D of the hot columns
 //   pend[NCOPY][2][H]     pending x / abar deltas of this CTA (fp64, smem atomics)
 // Hot reads come from the snapshot (an inconsistent read, like any other);
-// hot commits go to the pending arrays; every `period` CTA updates one warp
-// flushes pending -> global with one RED per (column, field) and refreshes
-// the snapshot.  Cuts same-sector L2 atomics on the Zipf head by ~period x.
+// hot commits go to the pending arrays; each warp, after every `period` of
+// its own updates, flushes the CTA's pending -> global with one RED per dirty
+// (column, field) and refreshes the snapshot (~one flush per `period` CTA
+// updates).  Cuts same-sector L2 atomics on the Zipf head by ~period x.
 constexpr int NCOPY = 2;
 
 struct HotView {
@@ -143,6 +146,12 @@ struct HotView {
 __device__ __forceinline__ HotView hot_view(double *base, int H)
 {
     return HotView{base, base + H, base + 2 * H, base + 3 * H, H};
+}
+
+__device__ __forceinline__ void mark_dirty(unsigned *dirty, int slot)
+{
+    unsigned *w = dirty + (slot & 31), b = 1u << (slot >> 5);
+    if (!(*(volatile unsigned *)w & b)) atomicOr(w, b);
 }
 
 __device__ __forceinline__ double smem_take(double *p)
@@ -158,7 +167,7 @@ __device__ __forceinline__ double smem_take(double *p)
 constexpr int HOT_PER_LANE = 8;  // H <= 256
 constexpr int HOT_MAX = 32 * HOT_PER_LANE;
 
-__device__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
+__device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
 {
     unsigned m = atomicExch(dirty + lane, 0u);
     while (m) {
@@ -172,7 +181,7 @@ __device__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int
             dx += smem_take(h.pend + (2 * c) * h.H + s);
             dab += smem_take(h.pend + (2 * c + 1) * h.H + s);
         }
-        double *g = a.coord + 4 * (int64_t)s;
+        double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
         if (dx != 0.0) red_add(g, dx);
         if (dab != 0.0) red_add(g + 1, dab);
     }
@@ -183,7 +192,7 @@ __device__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             int s = lane + 32 * (k0 + k);
-            if (s < h.H) v[k] = ld_cg2(a.coord + 4 * (int64_t)s);  // program order: sees our REDs
+            if (s < h.H) v[k] = ld_cg2(a.coord + 4 * ((int64_t)s << a.hot_shift));  // program order: sees our REDs
         }
 #pragma unroll
         for (int k = 0; k < 4; k++) {
@@ -202,34 +211,25 @@ template <typename VT, int NCH>
 __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, int k, int lane, const HotView &h,
                                         double *px, double *pab, unsigned *dirty)
 {
-    int colr[NCH];
+    int colr[NCH], slot[NCH];
     double vr[NCH], xr[NCH], abr[NCH], dr[NCH];
     double part = 0.0;
+    const int hmask = (1 << a.hot_shift) - 1, hlim = h.H << a.hot_shift;
 #pragma unroll
     for (int c = 0; c < NCH; c++) {
         int e = c * 32 + lane;
         colr[c] = -1;
+        slot[c] = -1;
         if (e < k) {
             int col = __ldg(a.col + lo + e);
             colr[c] = col;
             vr[c] = rv<VT>(a.val, lo + e);
-            if (col < h.H) {
-                if (a.hot_own & 2) {  // live L2 read of the hot cell (writes still aggregated)
-                    double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
-                    xr[c] = xa.x;
-                    abr[c] = xa.y;
-                } else {
-                    xr[c] = h.x[col];
-                    abr[c] = h.ab[col];
-                }
-                dr[c] = h.d[col];
-                if (a.hot_own & 1) {
-#pragma unroll
-                    for (int q = 0; q < NCOPY; q++) {
-                        xr[c] += h.pend[2 * q * h.H + col];
-                        abr[c] += h.pend[(2 * q + 1) * h.H + col];
-                    }
-                }
+            if (col < hlim && (col & hmask) == 0) slot[c] = col >> a.hot_shift;
+            if (slot[c] >= 0) {
+                const int sl = slot[c];
+                xr[c] = h.x[sl];
+                abr[c] = h.ab[sl];
+                dr[c] = h.d[sl];
             } else {
                 double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
                 xr[c] = xa.x;
@@ -249,12 +249,12 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
         if (colr[c] >= 0) {
             double v = dr[c] * (abr[c] + a.lambda1 * xr[c]);
             v += ds * vr[c];
-            double g = step_of(a, dr[c]);
+            double g = slot[c] >= 0 ? a.gamma * fmin(1.0, a.kappa_hot * dr[c]) : step_of(a, dr[c]);
             double u = xr[c] - g * v;
             double z = prox_sep(a.pen, u, g * dr[c], a.lam2, a.lo, a.hi);
-            if (colr[c] < h.H) {
-                atomicAdd(px + colr[c], z - xr[c]);
-                atomicOr(dirty + (colr[c] & 31), 1u << (colr[c] >> 5));
+            if (slot[c] >= 0) {
+                atomicAdd(px + slot[c], z - xr[c]);
+                mark_dirty(dirty, slot[c]);
             } else {
                 commit_x(a, colr[c], xr[c], z);
             }
@@ -266,9 +266,9 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
     for (int c = 0; c < NCH; c++) {
         if (colr[c] >= 0) {
             if (a.det) a.coord[4 * (int64_t)colr[c] + 1] = abr[c] + t * vr[c];
-            else if (colr[c] < h.H) {
-                atomicAdd(pab + colr[c], t * vr[c]);
-                atomicOr(dirty + (colr[c] & 31), 1u << (colr[c] >> 5));
+            else if (slot[c] >= 0) {
+                atomicAdd(pab + slot[c], t * vr[c]);
+                mark_dirty(dirty, slot[c]);
             }
             else red_add(a.coord + 4 * (int64_t)colr[c] + 1, t * vr[c]);
         }
@@ -491,28 +491,41 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
     // shared layout: [hot staging (hot_doubles) | CTA update counter + dirty[32] (17 doubles) | per-warp scratch]
     HotView h = hot_view(smem_dyn, a.H);
-    unsigned *upd = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
-    unsigned *dirty = upd + 2;
+    unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
     Scratch S{};
-    if (a.stride > 0) {
-        const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
-        double *base = a.smem ? smem_dyn + hdr + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
-        S = carve(base, a.M, a.GB);
+    if constexpr (MAXT <= 256) {  // the 1024-thread variant only runs rows of <= 32 nonzeros
+        if (a.stride > 0) {
+            const int hdr = a.H > 0 ? a.hot_doubles + 16 : 0;
+            double *base = a.smem ? smem_dyn + hdr + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
+            S = carve(base, a.M, a.GB);
+        }
     }
     if (a.H > 0) {
         for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
-            double2 v = ld_cg2(a.coord + 4 * (int64_t)s);
+            const double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            double2 v = ld_cg2(g);
             h.x[s] = v.x;
             h.ab[s] = v.y;
-            h.d[s] = __ldg(a.coord + 4 * (int64_t)s + 2);
+            h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 34) upd[threadIdx.x] = 0u;
+        if (threadIdx.x < 32) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
-    uint64_t slot = 0, slot_end = 0;
+    // async work split (asynchronous.py:125-128 split_iterations): warp gw owns
+    // the contiguous slot range [s0, s1) of this call; no atomics on the way.
+    // With batch > 0 warps instead claim `batch` slots at a time from the
+    // device counter (dynamic scheduling; diagnostics).
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t q = a.count / nwarps, r = a.count % nwarps;
+    uint64_t slot = (uint64_t)(gw * q + min(gw, r));
+    uint64_t slot_end = a.batch > 0 ? 0 : slot + (uint64_t)(q + (gw < r ? 1 : 0));
+    if (a.batch > 0) slot = 0;
     int64_t t = 0;
+    // each warp flushes the CTA's pending hot deltas after every `period` of its
+    // own updates (staggered start), i.e. about once per `period` CTA updates
+    int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, (int)(blockDim.x >> 5)) : 0;
     while (true) {
         int64_t i;
         if (a.det) {
@@ -521,6 +534,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
             t++;
         } else {
             if (slot >= slot_end) {
+                if (a.batch <= 0) break;
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)a.batch);
                 base = __shfl_sync(FULL, base, 0);
@@ -528,24 +542,30 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
                 slot = base;
                 slot_end = min((uint64_t)(base + a.batch), (uint64_t)a.count);
             }
-            i = sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n);
+            uint64_t sl = a.scramble ? (slot * a.scramble) % (uint64_t)a.count : slot;
+            i = sample_row(a.seed, a.slot_base + sl, (uint64_t)a.n);
             slot++;
         }
         int64_t lo = rp<PT>(a.row_ptr, i);
         int k = (int)(rp<PT>(a.row_ptr, i + 1) - lo);
-        constexpr int NCH = MAXT > 256 ? 1 : NCH_MAX;
-        if (PART == PS_PART_SINGLETON && k <= NCH * 32) row_reg<VT, NCH>(a, i, lo, k, lane, h, px, pab, dirty);
-        else row_slots<VT, PART>(a, i, lo, k, lane, S);
+        if constexpr (MAXT > 256) {
+            row_reg<VT, 1>(a, i, lo, k, lane, h, px, pab, dirty);
+        } else {
+            if (PART == PS_PART_SINGLETON && k <= NCH_MAX * 32) row_reg<VT, NCH_MAX>(a, i, lo, k, lane, h, px, pab, dirty);
+            else row_slots<VT, PART>(a, i, lo, k, lane, S);
+        }
         if (a.det) {
             __threadfence();
             __syncwarp();
         }
-        if (a.H > 0) {
-            unsigned old = 0;
-            if (lane == 0) old = atomicAdd(upd, 1u);
-            old = __shfl_sync(FULL, old, 0);
-            if ((old + 1) % (unsigned)a.period == 0) hot_flush(a, h, dirty, lane, true);
+        if (a.H > 0 && --until_flush == 0) {
+            hot_flush(a, h, dirty, lane, true);
+            until_flush = a.period;
         }
+    }
+    if (!a.det && a.batch <= 0 && lane == 0) {  // progress counter (asynchronous.py:156-165)
+        int64_t mine = q + (gw < r ? 1 : 0);
+        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
     }
     if (a.H > 0) {  // every warp of the CTA has left the loop: final flush
         __syncthreads();
@@ -574,7 +594,7 @@ static int scratch_layout(const ps_csr_t *csr, const ps_part_t *part, int *M, in
 static bool needs_scratch(const ps_csr_t *csr, const ps_part_t *part, bool big = false)
 {
     if (part->kind != PS_PART_SINGLETON) return true;
-    return part->max_slots > (big ? 1 : NCH_MAX) * 32;
+    return !big && part->max_slots > NCH_MAX * 32;
 }
 
 extern "C" int64_t ps_scratch_bytes(const ps_csr_t *csr, const ps_part_t *part, int32_t warps)
@@ -631,11 +651,14 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : 8);
-    bool big = part->kind == PS_PART_SINGLETON && wpc > 8;
+    // default: singleton rows of <= 32 nonzeros run one 24-warp CTA per SM (fewest
+    // hot-flush agents, full register budget); everything else 8-warp CTAs
+    const bool can_big = part->kind == PS_PART_SINGLETON && part->max_slots <= 32;
+    int wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : (can_big ? 24 : 8));
+    bool big = can_big && wpc > 8;
     L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
     L->kernel = pick_kernel(csr, part->kind, big);
-    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
+    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 16) * 8 : 0;
     L->smem_flag = 0;
     L->stride = L->M = L->GB = 0;
     L->gscratch_bytes = 0;
@@ -689,8 +712,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     if (sched->count < 0) return ps_fail(PS_EINVAL, "negative update count");
     if (sched->count == 0) return PS_OK;
     const bool det = sched->samples != nullptr;
-    if (!det && (!sched->counter || sched->batch < 1))
-        return ps_fail(PS_EINVAL, "async mode needs a device counter and batch >= 1");
+    if (!det && !sched->counter) return ps_fail(PS_EINVAL, "async mode needs a device counter");
 
     KArgs a{};
     a.row_ptr = csr->row_ptr;
@@ -718,7 +740,12 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     a.gamma = prm->gamma;
     a.samples = sched->samples;
     a.count = sched->count;
-    a.seed = sched->seed;
+    {  // splitmix64(seed), host side
+        uint64_t z = sched->seed + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        a.seed = z ^ (z >> 31);
+    }
     a.slot_base = sched->slot_base;
     a.counter = sched->counter;
     a.batch = sched->batch;
@@ -729,12 +756,22 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     if (r) return r;
     a.H = L.H;
     a.hot_doubles = L.hot_doubles;
-    a.hot_own = sched->reserved & 3;
-    a.period = sched->hot_period > 0 ? sched->hot_period : std::max(1, L.wpc / 2);
+    a.hot_shift = std::max(0, (int)sched->hot_shift);
+    a.scramble = 0;
+    if (sched->flags & 4) {  // diagnostics: permute the slot order within the call
+        uint64_t m = 1000003ull;  // prime
+        while ((uint64_t)sched->count % m == 0) m += 2;
+        a.scramble = m % (uint64_t)sched->count ? m : 1;
+    }
+    a.period = sched->hot_period > 0 ? sched->hot_period : 8;
     // effective delay: in-flight warps + the staleness of the hot snapshot
     // (up to period * ctas updates between a CTA's refreshes)
     double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);
     a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
+    {  // diagnostics: flags bits 8..15 = extra divisor of the hot columns' kappa
+        int div = (sched->flags >> 8) & 0xff;
+        a.kappa_hot = a.kappa / (double)(div > 0 ? div : 1);
+    }
     a.stride = L.stride;
     a.M = L.M;
     a.GB = L.GB;

@@ -50,7 +50,7 @@ class DeviceProblem:
     """
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
-                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, _labels=None):
+                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, hot_stride=32, _labels=None):
         torch = _torch()
         _lib.require_device()
         self.torch = torch
@@ -91,9 +91,9 @@ class DeviceProblem:
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
             # ---- partition (+ hot-column renumbering for singleton layouts)
             self._setup_partition(partition)
-            self.H, self.perm, self.perm_np = 0, None, None
+            self.H, self.hot_shift, self.perm, self.perm_np = 0, 0, None, None
             if self.part_kind == "singleton" and hot_max > 0 and self.n >= 4096:
-                self._hot_layout(int(hot_max), float(hot_min_frac))
+                self._hot_layout(int(hot_max), float(hot_min_frac), int(hot_stride))
             # ---- state
             self.coord = torch.zeros((self.p, 4), dtype=torch.float64, device=dev)
             self.alpha = torch.zeros(self.n, dtype=torch.float64, device=dev)
@@ -161,18 +161,19 @@ class DeviceProblem:
         self.part.blk_count = self.blk_count.data_ptr()
         self.part.blk_weight = self.blk_weight.data_ptr()
 
-    def _hot_layout(self, hot_max, min_frac):
+    def _hot_layout(self, hot_max, min_frac, stride):
         """ps_hot_layout: the most frequent columns become [0, H) (staged in
         shared memory by the async kernel); the device CSR is remapped in place."""
         torch, dev = self.torch, self.device
         ws = torch.empty(self.p, dtype=torch.int32, device=dev)
         self.perm = torch.empty(self.p, dtype=torch.int32, device=dev)
         self.inv = torch.empty(self.p, dtype=torch.int32, device=dev)
-        H = ctypes.c_int32(0)
-        _lib.check(_lib.load().ps_hot_layout(self.csr, self.col.data_ptr(), hot_max, min_frac, ws.data_ptr(),
-                                             self.perm.data_ptr(), self.inv.data_ptr(), ctypes.byref(H),
-                                             _lib.stream_ptr()))
+        H, S = ctypes.c_int32(0), ctypes.c_int32(stride)
+        _lib.check(_lib.load().ps_hot_layout(self.csr, self.col.data_ptr(), hot_max, min_frac, ctypes.byref(S),
+                                             ws.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),
+                                             ctypes.byref(H), _lib.stream_ptr()))
         self.H = H.value
+        self.hot_shift = S.value.bit_length() - 1
         self.perm_np = self.perm.cpu().numpy().astype(np.int64)
 
     def _to_stored(self, v):
@@ -203,11 +204,12 @@ class DeviceProblem:
                                               self.counter.data_ptr(), _lib.stream_ptr(stream)))
         self.slot_base = 0
 
-    def _sched(self, count, samples=None, seed=0, batch=32, ctas=0, warps_per_cta=0, contention=0.0,
+    def _sched(self, count, samples=None, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=0.0,
                hot=True, hot_period=0, flags=0):
         return _lib.Sched(samples, int(count), int(seed) & (2 ** 64 - 1), int(self.slot_base),
                           self.counter.data_ptr(), int(batch), int(ctas), int(warps_per_cta),
-                          int(self.H if hot else 0), float(contention), int(hot_period), int(flags))
+                          int(self.H if hot else 0), float(contention), int(hot_period), int(flags),
+                          int(self.hot_shift), 0)
 
     def launch_config(self, sched):
         c, w, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
@@ -240,7 +242,7 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self._keep = s
 
-    def run_async(self, count, gamma, seed=0, batch=32, ctas=0, warps_per_cta=0, contention=2.0, hot=True,
+    def run_async(self, count, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=2.0, hot=True,
                   hot_period=0, flags=0, stream=None):
         """`count` lock-free updates (asynchronous.py:131-210), continuing the
         sampler stream where the previous call stopped.  ``contention`` = c of

@@ -43,7 +43,7 @@ def test_struct_layouts_match_header():
     # keeps 64-bit fields first so the layouts are padding-free where it matters
     assert ctypes.sizeof(_lib.Csr) == 8 * 3 + 8 * 4 + 4 * 2
     assert ctypes.sizeof(_lib.Params) == 8 + 8 * 5
-    assert ctypes.sizeof(_lib.Sched) == 8 * 5 + 4 * 4 + 8 + 4 * 2
+    assert ctypes.sizeof(_lib.Sched) == 8 * 5 + 4 * 4 + 8 + 4 * 4
 
 
 def test_solver_without_device_fails_loudly():

@@ -33,10 +33,9 @@ def run(tag, phases):
                       "gap": [float(f"{g:.2e}") for g in gaps[4::5]], "final": gaps[-1],
                       "abar_drift": drift, "residual": res}), flush=True)
 
-for wpc in (32, 16):
-    for hp in (4, 8, 16, 32):
-        run(f"wpc{wpc}_hp{hp}_c2", [(30, dict(ctas=148, warps_per_cta=wpc, contention=2.0, hot_period=hp))])
-run("wpc32_hp8_c4", [(30, dict(ctas=148, warps_per_cta=32, contention=4.0, hot_period=8))])
-run("wpc32_hp8_c1", [(30, dict(ctas=148, warps_per_cta=32, contention=1.0, hot_period=8))])
-run("wpc32_hp8_c2_live", [(30, dict(ctas=148, warps_per_cta=32, contention=2.0, hot_period=8, flags=2))])
-run("nohot_wpc32", [(30, dict(ctas=148, warps_per_cta=32, contention=2.0, hot=False))])
+B = dict(ctas=148, warps_per_cta=32)
+for hp in (8, 16, 32):
+    run(f"w32_hp{hp}_b4_c2", [(30, dict(B, contention=2.0, hot_period=hp, batch=4))])
+run("w16_hp16_b4_c2", [(30, dict(ctas=148, warps_per_cta=16, contention=2.0, hot_period=16, batch=4))])
+run("w24_hp16_b4_c2", [(30, dict(ctas=148, warps_per_cta=24, contention=2.0, hot_period=16, batch=4))])
+run("w16_hp16_b4_c4", [(30, dict(ctas=148, warps_per_cta=16, contention=4.0, hot_period=16, batch=4))])
