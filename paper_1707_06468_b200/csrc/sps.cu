@@ -138,14 +138,18 @@ __device__ __forceinline__ void commit_abar(const KArgs &a, int64_t c, double in
 // updates).  Cuts same-sector L2 atomics on the Zipf head by ~period x.
 constexpr int NCOPY = 2;
 
+// shared-memory layout of the staging area (doubles):
+//   [0, 2H)            snapshot pairs (x_s, abar_s), 16 B each (cp.async target)
+//   [2H, 3H)           D_s
+//   [3H, 3H+2*NCOPY*H) pending x / abar deltas, NCOPY copies
 struct HotView {
-    double *x, *ab, *d, *pend;
+    double *xab, *d, *pend;
     int H;
 };
 
 __device__ __forceinline__ HotView hot_view(double *base, int H)
 {
-    return HotView{base, base + H, base + 2 * H, base + 3 * H, H};
+    return HotView{base, base + 2 * H, base + 3 * H, H};
 }
 
 __device__ __forceinline__ void mark_dirty(unsigned *dirty, int slot)
@@ -162,48 +166,52 @@ __device__ __forceinline__ double smem_take(double *p)
 // flush this CTA's pending deltas to global, then refresh the snapshot.
 // Lane l owns slots l, l+32, ... (HOT_PER_LANE of them; the hottest columns
 // spread over lanes); `dirty[l]` has bit k set when slot l+32k has pending
-// deltas.  REDs are fire-and-forget; the refresh loads are issued together so
-// one L2 latency covers all of a lane's slots.
-constexpr int HOT_PER_LANE = 8;  // H <= 256
+// deltas.  REDs are fire-and-forget and the snapshot refresh is a set of
+// cp.async global->shared copies, so the flushing warp never waits on memory.
+constexpr int HOT_PER_LANE = 32;  // H <= 1024 (dirty bitmask: one 32-bit word per lane)
 constexpr int HOT_MAX = 32 * HOT_PER_LANE;
+constexpr int HOT_TIER0 = 128;  // slots refreshed on every flush
 
 __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
 {
+    extern __shared__ double smem_dyn[];  // h.* point into it: use explicit shared addressing
+    const int H = h.H;
+    double *pend = smem_dyn + 3 * H;
     unsigned m = atomicExch(dirty + lane, 0u);
     while (m) {
         int k = __ffs(m) - 1;
         m &= m - 1;
         int s = lane + 32 * k;
-        if (s >= h.H) continue;
+        if (s >= H) continue;
         double dx = 0.0, dab = 0.0;
 #pragma unroll
         for (int c = 0; c < NCOPY; c++) {
-            dx += smem_take(h.pend + (2 * c) * h.H + s);
-            dab += smem_take(h.pend + (2 * c + 1) * h.H + s);
+            dx += smem_take(pend + (2 * c) * H + s);
+            dab += smem_take(pend + (2 * c + 1) * H + s);
         }
         double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
         if (dx != 0.0) red_add(g, dx);
         if (dab != 0.0) red_add(g + 1, dab);
     }
     if (!refresh) return;
-#pragma unroll 1
-    for (int k0 = 0; k0 < HOT_PER_LANE; k0 += 4) {
-        double2 v[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            int s = lane + 32 * (k0 + k);
-            if (s < h.H) v[k] = ld_cg2(a.coord + 4 * ((int64_t)s << a.hot_shift));  // program order: sees our REDs
-        }
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            int s = lane + 32 * (k0 + k);
-            if (s < h.H) {
-                h.x[s] = v[k].x;
-                h.ab[s] = v[k].y;
-            }
+    // tiered refresh: the HOT_TIER0 hottest slots every flush, the rest a
+    // rotating quarter per flush (their columns change ~p_j times slower)
+    unsigned rot = 0;
+    if (lane == 0) rot = atomicAdd(dirty + 32, 1u);
+    rot = __shfl_sync(FULL, rot, 0) & 3u;
+#pragma unroll 4
+    for (int k = 0; k < HOT_PER_LANE; k++) {
+        int s = lane + 32 * k;
+        if (s < H && (k < HOT_TIER0 / 32 || (k & 3) == (int)rot)) {
+            unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dyn + 2 * s);
+            const double *src = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
         }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
+
+__device__ __forceinline__ void hot_async_drain() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // SINGLETON fast path: k <= NCH*32, everything in registers.
@@ -227,8 +235,9 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
             if (col < hlim && (col & hmask) == 0) slot[c] = col >> a.hot_shift;
             if (slot[c] >= 0) {
                 const int sl = slot[c];
-                xr[c] = h.x[sl];
-                abr[c] = h.ab[sl];
+                double2 v = reinterpret_cast<const double2 *>(h.xab)[sl];
+                xr[c] = v.x;
+                abr[c] = v.y;
                 dr[c] = h.d[sl];
             } else {
                 double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
     Scratch S{};
     if constexpr (MAXT <= 256) {  // the 1024-thread variant only runs rows of <= 32 nonzeros
         if (a.stride > 0) {
-            const int hdr = a.H > 0 ? a.hot_doubles + 16 : 0;
+            const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
             double *base = a.smem ? smem_dyn + hdr + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
             S = carve(base, a.M, a.GB);
         }
@@ -504,13 +513,11 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
     if (a.H > 0) {
         for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
             const double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
-            double2 v = ld_cg2(g);
-            h.x[s] = v.x;
-            h.ab[s] = v.y;
+            reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 32) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     // async work split (asynchronous.py:125-128 split_iterations): warp gw owns
@@ -568,12 +575,211 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
         if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
     }
     if (a.H > 0) {  // every warp of the CTA has left the loop: final flush
+        hot_async_drain();
         __syncthreads();
         if (wib == 0) {
-            dirty[lane] = 0xffffffffu >> (32 - HOT_PER_LANE);  // flush every slot
+            dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));  // every slot
             __syncwarp();
             hot_flush(a, h, dirty, lane, false);
         }
+        hot_async_drain();
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fast async kernel: SINGLETON rows of <= 32 nonzeros (BASELINE configs 2-4).
+// Same per-update arithmetic as row_reg, specialised on loss / penalty, with
+// a software pipeline across updates:
+//   * the NEXT sample's CSR row (row_ptr, columns, values, label) is fetched
+//     while the current update computes -- these reads do not touch x, so
+//     they shorten the dependent chain without adding staleness;
+//   * the alpha exchange of update t is consumed (abar credit) only after the
+//     state loads of update t+1 are issued, hiding its round trip.
+// One warp per in-flight sample; hot columns staged in shared memory.
+template <typename VT> struct RowRegs {
+    int64_t i;
+    int k, col;
+    VT val, y;  // raw (widened at use, so the prefetch is not forced to complete early)
+};
+
+template <typename VT, typename PT>
+__device__ __forceinline__ RowRegs<VT> fetch_row(const KArgs &a, int64_t i, int lane)
+{
+    RowRegs<VT> r;
+    r.i = i;
+    int64_t lo = rp<PT>(a.row_ptr, i);
+    r.k = (int)(rp<PT>(a.row_ptr, i + 1) - lo);
+    r.col = -1;
+    r.val = VT(0);
+    if (lane < r.k) {
+        r.col = __ldg(a.col + lo + lane);
+        r.val = __ldg(reinterpret_cast<const VT *>(a.val) + lo + lane);
+    }
+    r.y = __ldg(reinterpret_cast<const VT *>(a.y) + i);
+    return r;
+}
+
+template <int PEN> __device__ __forceinline__ double prox_t(const KArgs &a, double u, double eff)
+{
+    if (PEN == PS_PEN_L1) {
+        double thr = eff * a.lam2;
+        double m = fmax(fabs(u) - thr, 0.0);
+        return u > 0 ? m : (u < 0 ? -m : 0.0);
+    }
+    return prox_sep(a.pen, u, eff, a.lam2, a.lo, a.hi);
+}
+
+template <int LOSS> __device__ __forceinline__ double deriv_t(double z, double b)
+{
+    return loss_deriv(LOSS, z, b);
+}
+
+template <typename VT, typename PT, int LOSS, int PEN, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
+{
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int nwib = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * nwib + wib;
+    HotView h = hot_view(smem_dyn, a.H);
+    unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
+    double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
+    if (a.H > 0) {
+        for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
+            const double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
+            h.d[s] = __ldg(g + 2);
+        }
+        for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
+        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
+        __syncthreads();
+    }
+    const int64_t nwarps = (int64_t)gridDim.x * nwib;
+    const int64_t q = a.count / nwarps, rr = a.count % nwarps;
+    uint64_t slot = (uint64_t)(gw * q + min(gw, rr));
+    const uint64_t slot_end = slot + (uint64_t)(q + (gw < rr ? 1 : 0));
+    const int hmask = (1 << a.hot_shift) - 1, hlim = a.H << a.hot_shift;
+    const double inv_n = 1.0 / a.n_d;
+    int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, nwib) : 0;
+
+    // pending abar credit of the previous update
+    int pcol = -1, pslot = -1;
+    double pval = 0.0, pnw = 0.0, prep = 0.0;
+    bool pend_credit = false;
+
+    if (slot < slot_end) {
+        RowRegs<VT> cur = fetch_row<VT, PT>(a, sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n), lane);
+        while (true) {
+            // ---- state reads of the current update
+            const int col = cur.col;
+            int sl = -1;
+            double xh = 0.0, ab = 0.0, d = 0.0;
+            if (col >= 0) {
+                if (col < hlim && (col & hmask) == 0) sl = col >> a.hot_shift;
+                if (sl >= 0) {
+                    double2 v = reinterpret_cast<const double2 *>(h.xab)[sl];
+                    xh = v.x;
+                    ab = v.y;
+                    d = h.d[sl];
+                } else {
+                    double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
+                    xh = xa.x;
+                    ab = xa.y;
+                    d = __ldg(a.coord + 4 * (int64_t)col + 2);
+                }
+            }
+            double old = 0.0;
+            if (lane == 0) old = ld_cg(a.alpha + cur.i);
+            // ---- abar credit of the previous update (its exchange has returned by now)
+            if (pend_credit) {
+                double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+                if (pcol >= 0) {
+                    if (pslot >= 0) {
+                        atomicAdd(pab + pslot, t * pval);
+                        mark_dirty(dirty, pslot);
+                    } else {
+                        red_add(a.coord + 4 * (int64_t)pcol + 1, t * pval);
+                    }
+                }
+            }
+            // ---- prefetch the next sample's row (independent of the state)
+            const bool more = slot + 1 < slot_end;
+            slot++;
+            int64_t ni = more ? sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n) : cur.i;
+            int64_t nlo = rp<PT>(a.row_ptr, ni);
+            int nk = more ? (int)(rp<PT>(a.row_ptr, ni + 1) - nlo) : 0;
+            // ---- margin -> derivative -> prox
+            const double cval = widen(cur.val);
+            double margin = warp_sum(col >= 0 ? cval * xh : 0.0);
+            old = __shfl_sync(FULL, old, 0);
+            double nw = deriv_t<LOSS>(margin, widen(cur.y));
+            double ds = nw - old;
+            // next row's columns / values / label
+            RowRegs<VT> nxt;
+            nxt.i = ni;
+            nxt.k = nk;
+            nxt.col = -1;
+            nxt.val = VT(0);
+            if (lane < nk) {
+                nxt.col = __ldg(a.col + nlo + lane);
+                nxt.val = __ldg(reinterpret_cast<const VT *>(a.val) + nlo + lane);
+            }
+            nxt.y = more ? __ldg(reinterpret_cast<const VT *>(a.y) + ni) : VT(0);
+            if (col >= 0) {
+                double v = d * (ab + a.lambda1 * xh);
+                v += ds * cval;
+                double g = a.gamma * fmin(1.0, (sl >= 0 ? a.kappa_hot : a.kappa) * d);
+                double u = xh - g * v;
+                double z = prox_t<PEN>(a, u, g * d);
+                if (sl >= 0) {
+                    atomicAdd(px + sl, z - xh);
+                    mark_dirty(dirty, sl);
+                } else {
+                    red_add(a.coord + 4 * (int64_t)col, z - xh);
+                }
+            }
+            // ---- alpha_i <-> new (consumed next iteration)
+            double rep = 0.0;
+            if (lane == 0) rep = atomic_exch(a.alpha + cur.i, nw);
+            pcol = col;
+            pslot = sl;
+            pval = cval;
+            pnw = nw;
+            prep = rep;
+            pend_credit = true;
+            if (a.H > 0 && --until_flush == 0) {
+                hot_flush(a, h, dirty, lane, true);
+                until_flush = a.period;
+            }
+            if (!more) break;
+            cur = nxt;
+        }
+        // last credit
+        double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+        if (pcol >= 0) {
+            if (pslot >= 0) {
+                atomicAdd(pab + pslot, t * pval);
+                mark_dirty(dirty, pslot);
+            } else {
+                red_add(a.coord + 4 * (int64_t)pcol + 1, t * pval);
+            }
+        }
+    }
+    if (lane == 0) {
+        int64_t mine = q + (gw < rr ? 1 : 0);
+        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
+    }
+    if (a.H > 0) {
+        hot_async_drain();
+        __syncthreads();
+        if (wib == 0) {
+            dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));
+            __syncwarp();
+            hot_flush(a, h, dirty, lane, false);
+        }
+        hot_async_drain();
     }
 }
 
@@ -613,6 +819,24 @@ template <typename VT, typename PT> static void *kernel_ptr_big()
 {
     return (void *)sps_kernel<VT, PT, PS_PART_SINGLETON, 1024>;
 }
+constexpr int FAST_T = 768;
+template <typename VT, typename PT> static void *kernel_ptr_fast(int loss, int pen)
+{
+    if (loss == PS_LOSS_LOGISTIC) {
+        if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, FAST_T>;
+        return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, FAST_T>;
+    }
+    if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, FAST_T>;
+    return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, FAST_T>;
+}
+static void *pick_fast(const ps_csr_t *csr, int loss, int pen)
+{
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) return kernel_ptr_fast<double, long long>(loss, pen);
+    if (f64) return kernel_ptr_fast<double, int>(loss, pen);
+    if (i64) return kernel_ptr_fast<float, long long>(loss, pen);
+    return kernel_ptr_fast<float, int>(loss, pen);
+}
 
 static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 {
@@ -638,12 +862,14 @@ static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 
 struct LaunchCfg {
     void *kernel;
+    bool fast;
     int ctas, wpc, smem_flag, stride, M, GB, H, hot_doubles;
     size_t smem;
     int64_t gscratch_bytes;
 };
 
-static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched, LaunchCfg *L)
+static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sched_t *sched, LaunchCfg *L,
+                         const ps_params_t *prm = nullptr)
 {
     const bool det = sched->samples != nullptr;
     L->H = (!det && part->kind == PS_PART_SINGLETON) ? std::min(HOT_MAX, std::max(0, (int)sched->hot_cols)) : 0;
@@ -658,7 +884,10 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     bool big = can_big && wpc > 8;
     L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
     L->kernel = pick_kernel(csr, part->kind, big);
-    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 16) * 8 : 0;
+    // the pipelined fast kernel: static split, 768-thread CTAs (flags bit 4 forces the generic one)
+    L->fast = !det && can_big && wpc == FAST_T / 32 && sched->batch <= 0 && !(sched->flags & 16);
+    if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, prm ? prm->penalty : PS_PEN_L1);
+    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
     L->smem_flag = 0;
     L->stride = L->M = L->GB = 0;
     L->gscratch_bytes = 0;
@@ -752,7 +981,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     a.det = det ? 1 : 0;
 
     LaunchCfg L;
-    int r = launch_config(csr, part, sched, &L);
+    int r = launch_config(csr, part, sched, &L, prm);
     if (r) return r;
     a.H = L.H;
     a.hot_doubles = L.hot_doubles;
@@ -763,7 +992,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
         while ((uint64_t)sched->count % m == 0) m += 2;
         a.scramble = m % (uint64_t)sched->count ? m : 1;
     }
-    a.period = sched->hot_period > 0 ? sched->hot_period : 8;
+    a.period = sched->hot_period > 0 ? sched->hot_period : 16;
     // effective delay: in-flight warps + the staleness of the hot snapshot
     // (up to period * ctas updates between a CTA's refreshes)
     double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);

@@ -7,7 +7,7 @@ sys.path.insert(0, str(ROOT))
 import paper_1707_06468_b200 as pb
 from paper_1707_06468_b200 import problems
 cfg = problems.config2(seed=0)
-dp = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True)
+dp = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True, hot_max=int(sys.argv[1]) if len(sys.argv) > 1 else 1024)
 n = dp.n
 gamma = pb.resolve_step_size("1/2L", dp.L, n, cfg["loss"].lambda1)
 fstar = json.loads((ROOT / "tests/golden/cfg2_fstar.json").read_text())["fstar"]
@@ -26,8 +26,7 @@ def run(tag, epochs=30, **kw):
     print(json.dumps({"tag": tag, "Mups": epochs * n / sum(ms) / 1e3, "ep_to_1e-6": hit, "kernel_ms_to_1e-6": t_hit,
                       "gap": [float(f"{g:.2e}") for g in gaps[4::5]]}), flush=True)
 
-for div in (1, 2, 4, 8, 16):
-    for c in (2.0, 4.0):
-        run(f"w24_hp8_c{c}_hotdiv{div}", ctas=148, warps_per_cta=24, contention=c, hot_period=8, flags=div << 8)
-run("w32_hp16_c4_hotdiv8", ctas=148, warps_per_cta=32, contention=4.0, hot_period=16, flags=8 << 8)
-run("w32_hp32_c4_hotdiv8", ctas=148, warps_per_cta=32, contention=4.0, hot_period=32, flags=8 << 8)
+print(json.dumps({"H": dp.H}))
+for hp in (8, 16, 32):
+    for c in (2.0, 3.0):
+        run(f"fast_w24_hp{hp}_c{c}", ctas=148, warps_per_cta=24, contention=c, hot_period=hp)

@@ -20,12 +20,21 @@ ap.add_argument("--warm", type=int, default=2)
 ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--per_launch", type=int, default=1)
 ap.add_argument("--grid", default="")
+ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--hot_max", type=int, default=256)
 a = ap.parse_args()
 cfg = problems.config2(seed=0)
-dp = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True)
+_dps = {}
+def get_dp(hm):
+    if hm not in _dps:
+        _dps.clear()
+        _dps[hm] = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True, hot_max=hm)
+    return _dps[hm]
+dp = get_dp(a.hot_max)
 gamma = pb.resolve_step_size("1/2L", dp.L, dp.n, cfg["loss"].lambda1)
 def one(a):
-    kw = dict(ctas=a.ctas, warps_per_cta=a.wpc, contention=a.c, hot=not a.nohot, hot_period=a.hp, batch=a.batch)
+    dp = get_dp(a.hot_max)
+    kw = dict(ctas=a.ctas, warps_per_cta=a.wpc, contention=a.c, hot=not a.nohot, hot_period=a.hp, batch=a.batch, flags=a.flags)
     dp.reset_state()
     for _ in range(a.warm):
         dp.run_async(dp.n * a.per_launch, gamma, seed=1, **kw)
