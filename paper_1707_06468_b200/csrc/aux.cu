@@ -668,15 +668,36 @@ __global__ void k_flag_sums(const int32_t *counts, int64_t p, int theta, int64_t
     }
 }
 
+// exclusive scan of nb per-chunk sums, one CTA (warp-shuffle scan per 1024 block)
 __global__ void k_scan_small(int64_t *sums, int nb)
 {
-    if (threadIdx.x == 0) {
-        int64_t run = 0;
-        for (int b = 0; b < nb; b++) {
-            int64_t v = sums[b];
-            sums[b] = run;
-            run += v;
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += blockDim.x) {
+        int b = base + threadIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        int64_t v = b < nb ? sums[b] : 0, x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
         }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int64_t t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t y = __shfl_up_sync(FULL, t, o);
+                if (lane >= o) t += y;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        int64_t incl = x + (w > 0 ? wsum[w - 1] : 0);
+        if (b < nb) sums[b] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += incl;
+        __syncthreads();
     }
 }
 
@@ -762,12 +783,12 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t ho
     int H = (int)h;
     int S = *stride_inout;
     while (S > 1 && (int64_t)S * H > p) S >>= 1;  // hot records at 0, S, 2S, ...
-    const int64_t chunk = 1 << 16;
+    const int64_t chunk = 1 << 12;
     int nb = (int)((p + chunk - 1) / chunk);
     int64_t *sums = nullptr;
     CK(cudaMallocAsync((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
     k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, p, theta, chunk, sums);
-    k_scan_small<<<1, 32, 0, st>>>(sums, nb);
+    k_scan_small<<<1, 1024, 0, st>>>(sums, nb);
     k_perm<<<nb, 32, 0, st>>>(counts_ws, p, theta, chunk, sums, H, S, perm, inv);
     if (nnz > 0) k_remap_cols<<<grid, 256, 0, st>>>(col_inout, nnz, perm);
     CK(cudaGetLastError(), "ps_hot_layout launch");

@@ -66,6 +66,7 @@ struct KArgs {
     int32_t hot_doubles;  // shared doubles used by the staging area
     int32_t hot_shift;    // hot slot r is stored at coordinate r << hot_shift
     uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
+    int32_t diag;         // diagnostics: bit5 hot abar credit direct to L2, bit6 hot x commit direct
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             if (pend_credit) {
                 double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
                 if (pcol >= 0) {
-                    if (pslot >= 0) {
+                    if (pslot >= 0 && !(a.diag & 32)) {
                         atomicAdd(pab + pslot, t * pval);
                         mark_dirty(dirty, pslot);
                     } else {
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                 double g = a.gamma * fmin(1.0, (sl >= 0 ? a.kappa_hot : a.kappa) * d);
                 double u = xh - g * v;
                 double z = prox_t<PEN>(a, u, g * d);
-                if (sl >= 0) {
+                if (sl >= 0 && !(a.diag & 64)) {
                     atomicAdd(px + sl, z - xh);
                     mark_dirty(dirty, sl);
                 } else {
@@ -759,7 +760,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         // last credit
         double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
         if (pcol >= 0) {
-            if (pslot >= 0) {
+            if (pslot >= 0 && !(a.diag & 32)) {
                 atomicAdd(pab + pslot, t * pval);
                 mark_dirty(dirty, pslot);
             } else {
@@ -987,12 +988,13 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     a.hot_doubles = L.hot_doubles;
     a.hot_shift = std::max(0, (int)sched->hot_shift);
     a.scramble = 0;
+    a.diag = sched->flags;
     if (sched->flags & 4) {  // diagnostics: permute the slot order within the call
         uint64_t m = 1000003ull;  // prime
         while ((uint64_t)sched->count % m == 0) m += 2;
         a.scramble = m % (uint64_t)sched->count ? m : 1;
     }
-    a.period = sched->hot_period > 0 ? sched->hot_period : 16;
+    a.period = sched->hot_period > 0 ? sched->hot_period : 8;
     // effective delay: in-flight warps + the staleness of the hot snapshot
     // (up to period * ctas updates between a CTA's refreshes)
     double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);

@@ -1,0 +1,140 @@
+"""Regularisation path: independent Sparse Proximal SAGA solves over a grid of
+penalty weights, sharded across GPUs (BASELINE config 5).
+
+The reference has no path driver (``gen_regularization``, problems.py:100-128,
+solves serially inside a bisection).  The path here:
+
+* lambdas: ``n_lambdas`` values log-spaced from lambda_max down to
+  ``ratio * lambda_max`` (group lambda_max = max_B ||grad_B f(0)||_2 for the
+  group penalty, problems.py:94-97's l1 formula otherwise);
+* sharding: one process per GPU (torchrun); lambdas are dealt to ranks
+  longest-expected-work-first (small lambda -> denser x -> slower), round
+  robin over the sorted list; the matrix is replicated on every rank;
+* no collective on the solve path; one ``all_gather_object`` of the per-lambda
+  summaries at the end (gloo or NCCL; NVLink carries it on a B200 node);
+* each solve reuses the rank's DeviceProblem: the state is reset and only the
+  penalty weight changes, so the CSR and the column statistics are uploaded
+  and computed once per rank.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+
+def lambda_grid(lam_max, n_lambdas=16, ratio=1e-3):
+    """Log-spaced from lam_max down to ratio * lam_max (inclusive)."""
+    if n_lambdas < 1:
+        raise ValueError("n_lambdas must be >= 1")
+    if n_lambdas == 1:
+        return [float(lam_max)]
+    return [float(lam_max * ratio ** (k / (n_lambdas - 1))) for k in range(n_lambdas)]
+
+
+def assign(lambdas, world):
+    """Rank -> list of lambda indices; longest expected work (smallest lambda) first."""
+    order = sorted(range(len(lambdas)), key=lambda k: lambdas[k])
+    shards = [[] for _ in range(world)]
+    for pos, k in enumerate(order):
+        shards[pos % world].append(k)
+    return shards
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist
+    except ImportError:
+        pass
+    return None
+
+
+def run_path(lambdas, solve, rank=None, world=None):
+    """Solve every lambda assigned to this rank with ``solve(lam) -> dict`` and
+    gather all summaries (every rank returns the full, lambda-ordered list)."""
+    dist = _dist()
+    if rank is None:
+        rank = dist.get_rank() if dist else 0
+    if world is None:
+        world = dist.get_world_size() if dist else 1
+    mine = assign(lambdas, world)[rank]
+    local = []
+    for k in mine:
+        t0 = time.perf_counter()
+        res = dict(solve(lambdas[k]))
+        res.update(index=k, lam=lambdas[k], rank=rank, seconds=time.perf_counter() - t0)
+        local.append(res)
+    if dist and world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, local)
+        allres = [r for part in gathered for r in part]
+    else:
+        allres = local
+    return sorted(allres, key=lambda r: r["index"])
+
+
+def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
+                  mode="async", contention=3.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
+    """A ``solve(lam)`` closure over one DeviceProblem (uploaded once)."""
+    from .device import DeviceProblem
+    from .penalties import GroupL2Penalty, L1Penalty
+    from .saga import resolve_step_size, worker_rng
+
+    pen0 = GroupL2Penalty(0.0) if penalty_kind == "group" else L1Penalty(0.0)
+    dp = DeviceProblem(data, loss, pen0, partition, device=device, drop_dead_blocks=True)
+    n = data.n_samples
+    gamma = resolve_step_size(step, dp.L, n, loss.lambda1 if loss.lambda1 > 0 else None)
+    samples = None
+    if mode == "deterministic":
+        samples = dp.torch.from_numpy(worker_rng(seed, 0).integers(0, n, size=epochs * n)).to(dp.device)
+
+    def solve(lam):
+        dp.lam2 = float(lam)
+        dp.reset_state()
+        if samples is not None:
+            dp.replay(samples, gamma)
+        else:
+            dp.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas,
+                         warps_per_cta=warps_per_cta)
+        parts = dp.objective_parts().cpu().numpy()
+        x = dp.x()
+        out = {"objective": float(parts.sum()), "nnz": int(np.count_nonzero(x)),
+               "norm": float(np.linalg.norm(x)), "updates": epochs * n}
+        if keep_x:
+            out["x"] = x
+        return out
+
+    solve.problem = dp
+    solve.gamma = gamma
+    return solve
+
+
+def lambda_max_for(data, partition, penalty_kind="group", device=None):
+    from .problems import group_lambda_max, lambda_max
+
+    if penalty_kind == "group":
+        return group_lambda_max(data, partition, device=device)
+    return lambda_max(data, device=device)
+
+
+def regularization_path(data, loss, partition, n_lambdas=16, ratio=1e-3, penalty_kind="group", epochs=30,
+                        step="1/2L", seed=0, mode="async", device=None, keep_x=False):
+    """Config 5 end to end on this rank's GPU (call under torchrun for N GPUs)."""
+    lam_max = lambda_max_for(data, partition, penalty_kind, device=device)
+    lams = lambda_grid(lam_max, n_lambdas, ratio)
+    solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
+                          keep_x=keep_x)
+    t0 = time.perf_counter()
+    res = run_path(lams, solve)
+    return {"lambda_max": lam_max, "lambdas": lams, "results": res, "seconds": time.perf_counter() - t0,
+            "total_updates": sum(r["updates"] for r in res)}
+
+
+def path_throughput(results, seconds):
+    tot = sum(r["updates"] for r in results)
+    return tot / seconds if seconds > 0 else math.inf

@@ -1,0 +1,51 @@
+"""λ-path (config 5 generator, scaled down) on the GPU: the device solver
+in deterministic mode reproduces the oracle per lambda (<= 1e-9), the async
+path reaches the deterministic objectives, and sparsity grows along the path."""
+
+import numpy as np
+import pytest
+
+import paper_1707_06468_b200 as pb
+from paper_1707_06468_b200 import lambda_path as lp
+from paper_1707_06468_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    return problems.config5(seed=1, n=4000, p=200_000)
+
+
+def test_group_lambda_max_zeroes_the_solution(cuda, cfg5):
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    lam_max = pb.group_lambda_max(d, part)
+    solve = lp.device_solver(d, loss, part, epochs=20, mode="deterministic")
+    assert solve(1.01 * lam_max)["nnz"] == 0
+    assert solve(0.5 * lam_max)["nnz"] > 0
+
+
+def test_deterministic_path_matches_oracle(cuda, cfg5):
+    from oracle import oracle as O
+
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    lams = lp.lambda_grid(pb.group_lambda_max(d, part), 4, 1e-2)
+    solve = lp.device_solver(d, loss, part, epochs=3, mode="deterministic", keep_x=True)
+    res = lp.run_path(lams, solve)
+    seq = pb.worker_rng(0, 0).integers(0, d.n_samples, size=3 * d.n_samples)
+    for r in res:
+        P = O.from_dataset(d, loss, pb.GroupL2Penalty(r["lam"]), part)
+        x, _, _ = P.run_sequential(solve.gamma, seq)
+        rel = np.max(np.abs(r["x"] - x)) / max(np.max(np.abs(x)), 1e-300)
+        assert rel <= 1e-9, (r["lam"], rel)
+        assert r["objective"] == pytest.approx(P.objective(x), rel=1e-12)
+
+
+def test_async_path_reaches_deterministic_objectives(cuda, cfg5):
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    lams = lp.lambda_grid(pb.group_lambda_max(d, part), 3, 1e-2)
+    det = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="deterministic"))
+    asy = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="async", ctas=8, warps_per_cta=4))
+    for a, b in zip(asy, det):
+        assert abs(a["objective"] - b["objective"]) <= 1e-6 * abs(b["objective"]), (a, b)
+    assert det[0]["nnz"] <= det[-1]["nnz"]

@@ -27,6 +27,5 @@ def run(tag, epochs=30, **kw):
                       "gap": [float(f"{g:.2e}") for g in gaps[4::5]]}), flush=True)
 
 print(json.dumps({"H": dp.H}))
-for hp in (8, 16, 32):
-    for c in (2.0, 3.0):
-        run(f"fast_w24_hp{hp}_c{c}", ctas=148, warps_per_cta=24, contention=c, hot_period=hp)
+for fl, tag in ((0, "both_staged"), (32, "abar_direct"), (64, "x_direct"), (96, "both_direct")):
+    run(f"{tag}_hp16_c3", ctas=148, warps_per_cta=24, contention=3.0, hot_period=16, flags=fl)
