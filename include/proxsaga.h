@@ -167,19 +167,22 @@ int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, v
 int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
             void *stream);
 
-/* Hot-column layout for SINGLETON partitions: columns present in at least
- * max(ceil(min_frac * n), theta) rows — theta the smallest threshold letting
- * at most hot_max columns qualify — are the H hot columns; hot rank r is
- * stored at index r * S (S = *stride_inout, a power of two, reduced until
- * S * H <= p) so consecutive hot records sit in different L2 slices; cold
- * columns fill the remaining indices in original order.  col_inout (the
- * device CSR's column array) is remapped in place.  perm[old] = new,
- * inv[new] = old (p int32 each); counts_ws: p int32 workspace.  The SPS
- * kernel stages hot columns in shared memory (sched->hot_cols = H,
- * sched->hot_shift = log2 S).  Synchronous; *H_out / *stride_inout host. */
-int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
-                  int32_t *stride_inout, int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out,
-                  void *stream);
+/* Hot layout (SINGLETON: unit = 1, columns; CONTIG: unit = G, whole blocks):
+ * units present in at least max(ceil(min_frac * n), theta) rows — theta the
+ * smallest threshold letting at most hot_max units qualify — are the H hot
+ * units; hot rank r is stored at unit index r * S (S = *stride_inout, a power
+ * of two, reduced until S * H <= #units) so consecutive hot records sit in
+ * different L2 slices; cold units fill the remaining indices in original
+ * order.  The device CSR's columns (col_inout) are remapped in place and each
+ * row re-sorted (values in val_inout move along), so rows stay strictly
+ * increasing (data.py:58-61).  perm[old coordinate] = new coordinate (p
+ * int32); counts_ws: ceil(p/unit) int32.  Coordinates are padded to whole
+ * units: *p_pad_out = ceil(p/unit) * unit (padding never touched).  The SPS
+ * kernel stages hot units in shared memory (sched->hot_cols = H,
+ * sched->hot_shift = log2 S).  Synchronous; H / S / p_pad are host memory. */
+int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_inout, int32_t unit,
+                  int32_t hot_max, double min_frac, int32_t *stride_inout, int32_t *counts_ws,
+                  int32_t *perm, int32_t *H_out, int64_t *p_pad_out, void *stream);
 
 /* Solver state to x0 = 0, abar = 0, alpha = 0, counter = 0 (D untouched):
  * saga.py:231-232. `counter` may be NULL. */

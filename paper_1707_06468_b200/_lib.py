@@ -94,7 +94,8 @@ def load():
         "ps_resync_average": (_i32, [_P(Csr), _vp, _vp, _vp]),
         "ps_prox": (_i32, [_P(Params), _vp, _vp, _i64, _vp, _vp]),
         "ps_state_reset": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
-        "ps_hot_layout": (_i32, [_P(Csr), _vp, _i32, _f64, _P(_i32), _vp, _vp, _vp, _P(_i32), _vp]),
+        "ps_hot_layout": (_i32, [_P(Csr), _vp, _vp, _i32, _i32, _f64, _P(_i32), _vp, _vp, _P(_i32), _P(_i64),
+                                 _vp]),
         "ps_coord_get_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
         "ps_coord_set_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
         "ps_coord_get": (_i32, [_vp, _i64, _i32, _vp, _vp]),

@@ -8,6 +8,7 @@
 // Reductions are deterministic: per-CTA partials, then one CTA sums them in
 // CTA order.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -738,37 +739,119 @@ __global__ void k_remap_cols(int32_t *col, int64_t nnz, const int32_t *perm)
         col[e] = perm[col[e]];
 }
 
-extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t hot_max, double min_frac,
-                             int32_t *stride_inout, int32_t *counts_ws, int32_t *perm, int32_t *inv, int32_t *H_out,
-                             void *stream)
+// distinct rows per unit (unit = 1: column counts; unit = G: block counts n_B).
+// Rows may be unsorted: a unit is counted at its first occurrence in the row.
+template <typename PT>
+__global__ void k_count_units(const void *row_ptr, const int32_t *col, int64_t n, int unit, int32_t *counts)
 {
-    if (!csr || !col_inout || !counts_ws || !perm || !inv || !H_out || !stride_inout)
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+    for (int64_t e = lo; e < hi; e++) {
+        int u = col[e] / unit;
+        bool first = true;
+        if (unit > 1)
+            for (int64_t f = lo; f < e && first; f++) first = (col[f] / unit) != u;
+        if (first) atomicAdd(counts + u, 1);
+    }
+}
+
+// coordinate permutation from the unit permutation: c -> perm_u[c / unit] * unit + c % unit
+__global__ void k_coord_perm(const int32_t *perm_u, int64_t p, int unit, int32_t *perm)
+{
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < p; c += (int64_t)gridDim.x * blockDim.x)
+        perm[c] = (int32_t)((int64_t)perm_u[c / unit] * unit + c % unit);
+}
+
+// restore strictly increasing columns per row after the remap (values move along):
+// warp bitonic sort for rows of <= 32 nonzeros, one-lane insertion sort otherwise
+template <typename VT, typename PT>
+__global__ void k_sort_rows(const void *row_ptr, int32_t *col, void *valp, int64_t n)
+{
+    VT *val = reinterpret_cast<VT *>(valp);
+    int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < n; i += nw) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        int k = (int)(hi - lo);
+        if (k <= 1) continue;
+        if (k <= 32) {
+            int c = lane < k ? col[lo + lane] : INT_MAX;
+            VT v = lane < k ? val[lo + lane] : VT(0);
+            for (int size = 2; size <= 32; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    int oc = __shfl_xor_sync(FULL, c, stride);
+                    VT ov = __shfl_xor_sync(FULL, v, stride);
+                    bool up = ((lane & size) == 0);
+                    bool lower = (lane & stride) == 0;
+                    bool take = lower ? (up ? oc < c : oc > c) : (up ? oc > c : oc < c);
+                    if (take) {
+                        c = oc;
+                        v = ov;
+                    }
+                }
+            }
+            if (lane < k) {
+                col[lo + lane] = c;
+                val[lo + lane] = v;
+            }
+        } else if (lane == 0) {
+            for (int64_t e = lo + 1; e < hi; e++) {
+                int c = col[e];
+                VT v = val[e];
+                int64_t f = e - 1;
+                while (f >= lo && col[f] > c) {
+                    col[f + 1] = col[f];
+                    val[f + 1] = val[f];
+                    f--;
+                }
+                col[f + 1] = c;
+                val[f + 1] = v;
+            }
+        }
+    }
+}
+
+extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_inout, int32_t unit,
+                             int32_t hot_max, double min_frac, int32_t *stride_inout, int32_t *counts_ws,
+                             int32_t *perm, int32_t *H_out, int64_t *p_pad_out, void *stream)
+{
+    if (!csr || !col_inout || !val_inout || !counts_ws || !perm || !H_out || !stride_inout || !p_pad_out)
         return ps_fail(PS_EINVAL, "null argument");
+    if (unit < 1) return ps_fail(PS_EINVAL, "unit must be >= 1");
     if (*stride_inout < 1 || (*stride_inout & (*stride_inout - 1)))
         return ps_fail(PS_EINVAL, "stride must be a power of two");
     if (hot_max < 0) return ps_fail(PS_EINVAL, "hot_max must be >= 0");
     cudaStream_t st = (cudaStream_t)stream;
-    int64_t p = csr->n_cols, n = csr->n_rows, nnz = csr->nnz;
+    const int64_t p = csr->n_cols, n = csr->n_rows, nnz = csr->nnz;
+    const int64_t nu = (p + unit - 1) / unit;
+    const bool i64 = csr->row_ptr_type == PS_I64, f64 = csr->value_type == PS_F64;
     int grid = sm_count() * 8;
-    CK(cudaMemsetAsync(counts_ws, 0, sizeof(int32_t) * p, st), "ps_hot_layout memset");
-    if (nnz > 0) k_count_cols<<<grid, 256, 0, st>>>(col_inout, nnz, counts_ws);
+    int rows_grid = (int)((n + 255) / 256);
+    CK(cudaMemsetAsync(counts_ws, 0, sizeof(int32_t) * nu, st), "ps_hot_layout memset");
+    if (nnz > 0) {
+        if (unit == 1) k_count_cols<<<grid, 256, 0, st>>>(col_inout, nnz, counts_ws);
+        else if (i64) k_count_units<long long><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
+        else k_count_units<int><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
+    }
     unsigned long long *cnt = nullptr;
     CK(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long), st), "ps_hot_layout alloc");
     auto count_ge = [&](int theta, unsigned long long *h) -> int {
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "ps_hot_layout memset");
-        k_count_ge<<<grid, 256, 0, st>>>(counts_ws, p, theta, cnt);
+        k_count_ge<<<grid, 256, 0, st>>>(counts_ws, nu, theta, cnt);
         CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "ps_hot_layout copy");
         CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
         return PS_OK;
     };
-    // smallest theta >= min_frac*n (and >= 1) with at most hot_max qualifying columns
+    // smallest theta >= min_frac*n (and >= 1) with at most hot_max qualifying units
     int lo = std::max(1, (int)std::ceil(min_frac * (double)n));
     unsigned long long h = 0;
     int r = count_ge(lo, &h);
     if (r) return r;
     int theta = lo;
     if (h > (unsigned long long)hot_max) {
-        int a = lo, b = (int)std::min<int64_t>(n + 1, INT32_MAX);  // count(b) == 0 <= hot_max
+        int a = lo, b = (int)std::min<int64_t>(n + 1, INT32_MAX);
         while (b - a > 1) {
             int mid = a + (b - a) / 2;
             r = count_ge(mid, &h);
@@ -782,21 +865,33 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, int32_t ho
     if (r) return r;
     int H = (int)h;
     int S = *stride_inout;
-    while (S > 1 && (int64_t)S * H > p) S >>= 1;  // hot records at 0, S, 2S, ...
+    while (S > 1 && (int64_t)S * H > nu) S >>= 1;  // hot units at 0, S, 2S, ... (unit indices)
     const int64_t chunk = 1 << 12;
-    int nb = (int)((p + chunk - 1) / chunk);
+    int nb = (int)((nu + chunk - 1) / chunk);
     int64_t *sums = nullptr;
+    int32_t *perm_u = nullptr, *inv_u = nullptr;
     CK(cudaMallocAsync((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
-    k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, p, theta, chunk, sums);
+    CK(cudaMallocAsync((void **)&perm_u, sizeof(int32_t) * std::max<int64_t>(nu, 1) * 2, st), "ps_hot_layout alloc");
+    inv_u = perm_u + nu;
+    k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, nu, theta, chunk, sums);
     k_scan_small<<<1, 1024, 0, st>>>(sums, nb);
-    k_perm<<<nb, 32, 0, st>>>(counts_ws, p, theta, chunk, sums, H, S, perm, inv);
-    if (nnz > 0) k_remap_cols<<<grid, 256, 0, st>>>(col_inout, nnz, perm);
+    k_perm<<<nb, 32, 0, st>>>(counts_ws, nu, theta, chunk, sums, H, S, perm_u, inv_u);
+    k_coord_perm<<<grid, 256, 0, st>>>(perm_u, p, unit, perm);
+    if (nnz > 0) {
+        k_remap_cols<<<grid, 256, 0, st>>>(col_inout, nnz, perm);
+        if (f64 && i64) k_sort_rows<double, long long><<<grid, 256, 0, st>>>(csr->row_ptr, col_inout, val_inout, n);
+        else if (f64) k_sort_rows<double, int><<<grid, 256, 0, st>>>(csr->row_ptr, col_inout, val_inout, n);
+        else if (i64) k_sort_rows<float, long long><<<grid, 256, 0, st>>>(csr->row_ptr, col_inout, val_inout, n);
+        else k_sort_rows<float, int><<<grid, 256, 0, st>>>(csr->row_ptr, col_inout, val_inout, n);
+    }
     CK(cudaGetLastError(), "ps_hot_layout launch");
+    CK(cudaFreeAsync(perm_u, st), "ps_hot_layout free");
     CK(cudaFreeAsync(sums, st), "ps_hot_layout free");
     CK(cudaFreeAsync(cnt, st), "ps_hot_layout free");
     CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
     *H_out = H;
     *stride_inout = S;
+    *p_pad_out = nu * unit;
     return PS_OK;
 }
 

@@ -50,7 +50,8 @@ class DeviceProblem:
     """
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
-                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, hot_stride=32, _labels=None):
+                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
+                 _labels=None):
         torch = _torch()
         _lib.require_device()
         self.torch = torch
@@ -91,11 +92,13 @@ class DeviceProblem:
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
             # ---- partition (+ hot-column renumbering for singleton layouts)
             self._setup_partition(partition)
-            self.H, self.hot_shift, self.perm, self.perm_np = 0, 0, None, None
-            if self.part_kind == "singleton" and hot_max > 0 and self.n >= 4096:
-                self._hot_layout(int(hot_max), float(hot_min_frac), int(hot_stride))
+            self.H, self.hot_shift, self.perm, self.perm_np, self.p_dev = 0, 0, None, None, self.p
+            self.hot_unit = 1 if self.part_kind == "singleton" else int(self.part.G)
+            if self.part_kind in ("singleton", "contiguous") and hot_max > 0 and self.n >= hot_min_rows:
+                units = hot_max if self.hot_unit == 1 else max(1, hot_max // self.hot_unit)
+                self._hot_layout(int(units), float(hot_min_frac), int(hot_stride))
             # ---- state
-            self.coord = torch.zeros((self.p, 4), dtype=torch.float64, device=dev)
+            self.coord = torch.zeros((self.p_dev, 4), dtype=torch.float64, device=dev)
             self.alpha = torch.zeros(self.n, dtype=torch.float64, device=dev)
             self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
             self.stats = _lib.Stats()
@@ -162,25 +165,30 @@ class DeviceProblem:
         self.part.blk_weight = self.blk_weight.data_ptr()
 
     def _hot_layout(self, hot_max, min_frac, stride):
-        """ps_hot_layout: the most frequent columns become [0, H) (staged in
-        shared memory by the async kernel); the device CSR is remapped in place."""
+        """ps_hot_layout: the most frequent units (columns, or whole blocks of a
+        contiguous partition) are stored strided at the front and staged in
+        shared memory by the async kernel; the device CSR is remapped and its
+        rows re-sorted in place; coordinates are padded to whole units."""
         torch, dev = self.torch, self.device
-        ws = torch.empty(self.p, dtype=torch.int32, device=dev)
+        G = self.hot_unit
+        ws = torch.empty(-(-self.p // G), dtype=torch.int32, device=dev)
         self.perm = torch.empty(self.p, dtype=torch.int32, device=dev)
-        self.inv = torch.empty(self.p, dtype=torch.int32, device=dev)
-        H, S = ctypes.c_int32(0), ctypes.c_int32(stride)
-        _lib.check(_lib.load().ps_hot_layout(self.csr, self.col.data_ptr(), hot_max, min_frac, ctypes.byref(S),
-                                             ws.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),
-                                             ctypes.byref(H), _lib.stream_ptr()))
-        self.H = H.value
+        H, S, pp = ctypes.c_int32(0), ctypes.c_int32(stride), ctypes.c_int64(0)
+        _lib.check(_lib.load().ps_hot_layout(self.csr, self.col.data_ptr(), self.val.data_ptr(), G, hot_max,
+                                             min_frac, ctypes.byref(S), ws.data_ptr(), self.perm.data_ptr(),
+                                             ctypes.byref(H), ctypes.byref(pp), _lib.stream_ptr()))
+        self.H = H.value * G          # staged coordinate slots
         self.hot_shift = S.value.bit_length() - 1
+        self.p_dev = int(pp.value)
+        self.csr.n_cols = self.p_dev
         self.perm_np = self.perm.cpu().numpy().astype(np.int64)
+        self.unit_perm_np = self.perm_np[::G] // G if G > 1 else self.perm_np
 
     def _to_stored(self, v):
-        """original-order vector -> stored (permuted) order"""
+        """original-order vector -> stored (permuted, padded) order"""
         if self.perm_np is None:
             return np.ascontiguousarray(v, dtype=np.float64)
-        out = np.empty(self.p)
+        out = np.zeros(self.p_dev)
         out[self.perm_np] = v
         return out
 
@@ -190,7 +198,7 @@ class DeviceProblem:
     def block_stats(self):
         c, w = self.blk_count.cpu().numpy(), self.blk_weight.cpu().numpy()
         if self.perm_np is not None:
-            c, w = c[self.perm_np], w[self.perm_np]
+            c, w = c[self.unit_perm_np], w[self.unit_perm_np]
         return c, w, self.stats
 
     # ------------------------------------------------------------------
@@ -200,7 +208,7 @@ class DeviceProblem:
 
     def reset_state(self, stream=None):
         """x0 = 0, alpha = 0, abar = 0 (PAPER.md:1195-1199 / saga.py:231-232)."""
-        _lib.check(_lib.load().ps_state_reset(self.coord.data_ptr(), self.p, self.alpha.data_ptr(), self.n,
+        _lib.check(_lib.load().ps_state_reset(self.coord.data_ptr(), self.p_dev, self.alpha.data_ptr(), self.n,
                                               self.counter.data_ptr(), _lib.stream_ptr(stream)))
         self.slot_base = 0
 
@@ -280,7 +288,7 @@ class DeviceProblem:
 
     def smooth_gradient_of(self, x):
         t = self.torch.from_numpy(self._to_stored(x)).to(self.device)
-        g = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
+        g = self.torch.empty(self.p_dev, dtype=self.torch.float64, device=self.device)
         _lib.check(_lib.load().ps_smooth_gradient(self.csr, self.params(), t.data_ptr(), 1, g.data_ptr(),
                                                   _lib.stream_ptr()))
         return self._to_original(g.cpu().numpy())
@@ -288,7 +296,7 @@ class DeviceProblem:
     def fixed_point_residual(self, gamma):
         """saga.py:299-317 at the current x."""
         if self._grad is None:
-            self._grad = self.torch.empty(self.p, dtype=self.torch.float64, device=self.device)
+            self._grad = self.torch.empty(self.p_dev, dtype=self.torch.float64, device=self.device)
         _lib.check(_lib.load().ps_fixed_point_residual(self.csr, self.part, self.params(gamma),
                                                        self.coord.data_ptr(), self._grad.data_ptr(),
                                                        self._out.data_ptr() + 24, _lib.stream_ptr()))

@@ -62,6 +62,33 @@ def test_deterministic_replay_matches_reference(cuda, name, small_cases, golden_
     assert np.allclose(dp.smooth_gradient_of(dp.x()), g[f"{name}__grad"], rtol=1e-12, atol=1e-15)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "acc_l1", "grp_contig", "grp_g1", "box_sq", "l1_ragged",
+                                  "grp_ragged_contig", "cfg2_small", "cfg5_small"])
+def test_deterministic_replay_through_hot_layout(cuda, name, small_cases, golden_small):
+    """Same parity with the hot-unit layout forced on (columns / whole blocks
+    renumbered and strided, rows re-sorted, coordinates padded to whole units)."""
+    case, g = small_cases[name], golden_small
+    dp = DeviceProblem(case["data"], case["loss"], case["penalty"], case["partition"],
+                       drop_dead_blocks=case["drop_dead"], hot_min_rows=0, hot_max=64, hot_stride=4)
+    assert dp.perm is not None and dp.H > 0
+    gamma = _gamma(case, dp)
+    counts, weights, _ = dp.block_stats()
+    assert np.array_equal(counts, g[f"{name}__nB"])
+    assert np.array_equal(weights, g[f"{name}__dB"])
+    seq = worker_rng(case["seed"], 0).integers(0, dp.n, size=case["steps"])
+    done = 0
+    for k, s in enumerate(case["segments"]):
+        dp.replay(seq[done:s], gamma)
+        done = s
+        ref = g[f"{name}__x"][k]
+        rel = np.max(np.abs(dp.x() - ref)) / max(np.max(np.abs(ref)), 1e-300)
+        assert rel <= DET_TOL, f"{name} segment {k}: rel {rel:.3e}"
+        assert dp.objective() == pytest.approx(float(g[f"{name}__obj"][k]), rel=1e-12)
+    assert np.max(np.abs(dp.abar() - g[f"{name}__abar"])) <= DET_TOL
+    assert dp.fixed_point_residual(gamma) == pytest.approx(float(g[f"{name}__residual"]), rel=1e-8, abs=1e-13)
+    assert np.allclose(dp.smooth_gradient_of(dp.x()), g[f"{name}__grad"], rtol=1e-12, atol=1e-15)
+
+
 def test_run_sequential_api_matches_reference_trace(cuda, small_cases, golden_small):
     """saga.py:217-259 contract on the acceptance instance (3 epochs, seed 2)."""
     case = small_cases["acc_l1"]
