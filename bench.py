@@ -155,46 +155,66 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
-def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
-    """Solve from zero with a device objective checkpoint every epoch; wall =
-    CUDA-event time of kernels + evaluations; log-linear
-    interpolation of the first crossing (asynchronous.py:213-230) on the
-    RELATIVE gap (F - F*)/|F*|."""
+def lambda_path_bench(rank, world, epochs):
+    """BASELINE config 5: 16-lambda group-lasso path (lambda_max .. 1e-3 lambda_max),
+    independent solves sharded over the ranks (lambda_path.assign), matrix
+    replicated, device-timed per rank, max over ranks; value = updates of all
+    solves / that time."""
     import torch
 
+    import paper_1707_06468_b200 as pb
+    from paper_1707_06468_b200 import lambda_path as lp
+    from paper_1707_06468_b200 import problems
+
+    cfg = problems.config5(seed=0)
+    d, part, loss = cfg["data"], cfg["partition"], cfg["loss"]
+    lam_max = pb.group_lambda_max(d, part)
+    lams = lp.lambda_grid(lam_max, 16, 1e-3)
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async")
+    dp = solve.problem
+    mine = lp.assign(lams, world)[rank]
+    n = d.n_samples
+    dp.lam2 = lams[mine[0]] if mine else lams[0]
     dp.reset_state()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    marks, objs = [], []
-    done = 0
-    evs = []
-    parts = []
-    while done < total:
-        dp.run_async(n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc)
-        done += n
-        pr = dp.objective_parts().clone()
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        evs.append(e)
-        parts.append(pr)
-        marks.append(done)
+    dp.run_async(n, solve.gamma, seed=99)  # warm-up
     torch.cuda.synchronize()
-    walls = [ev0.elapsed_time(e) / 1e3 for e in evs]
-    objs = [float(p.sum().item()) for p in parts]
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for k in mine:
+        dp.lam2 = lams[k]
+        dp.reset_state()
+        dp.run_async(epochs * n, solve.gamma, seed=k)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    res = {"lambdas": len(lams), "mine": len(mine), "ms": ms, "updates": len(mine) * epochs * n,
+           "bytes_per_update_est": 2 * 4 + 4 + 2 * 8 + 20 * (4 + 4) + 156.3 * 3 * 8 + 20 * 8 + 15.6 * 8}
+    return res
+
+
+def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
+    """Solve from zero with an objective checkpoint every epoch.  Checkpoints
+    are pipelined on the device (DeviceProblem.run_async_checkpointed: x
+    snapshot + objective on a side stream while the next epoch runs); the time
+    of a checkpoint is when its objective is known (CUDA events, evaluations
+    included).  Log-linear interpolation of the first crossing
+    (asynchronous.py:213-230) on the RELATIVE gap (F - F*)/|F*|."""
+    import math
+
+    dp.reset_state()
+    its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc)
     rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
     hit = None
     prev_rel, prev_w, prev_it = 1.0, 0.0, 0
-    for it, w, r in zip(marks, walls, rel):
+    for it, w, r in zip(its, walls, rel):
         if r <= target:
-            import math
-
             frac = math.log(prev_rel / target) / math.log(prev_rel / r) if prev_rel > r else 1.0
             hit = (prev_w + frac * (w - prev_w), (prev_it + frac * (it - prev_it)) / n)
             break
         prev_rel, prev_w, prev_it = r, w, it
     return {"target_rel_gap": target, "seconds": hit[0] if hit else None, "epochs": hit[1] if hit else None,
             "reached": hit is not None, "final_rel_gap": rel[-1], "epochs_run": total / n,
-            "fstar": fstar, "wall_incl_evals_s": walls[-1]}
+            "fstar": fstar, "wall_incl_evals_s": walls[-1], "checkpoints": "every epoch, pipelined on a side stream"}
 
 
 def main():
@@ -207,6 +227,8 @@ def main():
     ap.add_argument("--wpc", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-path", action="store_true")
+    ap.add_argument("--path-epochs", type=int, default=30)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -320,6 +342,21 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, epochs)
 
+    lpath = None
+    if not args.no_path:
+        del dp
+        torch.cuda.empty_cache()
+        lp_local = lambda_path_bench(rank, world, args.path_epochs)
+        t = torch.tensor([lp_local["ms"]], device="cuda")
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        upd = 16 * args.path_epochs * 100_000
+        lpath = {"workload": "config 5: group-lasso logistic n=1e5 p=1e7 G=10, 16 lambdas log-spaced "
+                             f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
+                             "sharded over ranks (longest-work-first), matrix replicated",
+                 "value": upd / (float(t.item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t.item()),
+                 "n_gpus": world, "algorithmic_bytes_per_update_est": lp_local["bytes_per_update_est"]}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -345,6 +382,7 @@ def main():
                     "seconds_per_call": float(np.mean(e2e_times))},
             "gpu_launches": 2 * args.steps,
             "cpu_baseline": cpu,
+            "lambda_path": lpath,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

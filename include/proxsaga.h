@@ -71,6 +71,7 @@ typedef struct ps_part {
     int32_t *row_g;          /* GENERAL: |T_i| */
     int32_t *spos;           /* GENERAL: nnz, ext slot of each nonzero */
     int32_t max_slots;       /* set by ps_prepare: max ext slots over rows */
+    int32_t max_row_nnz;     /* set by ps_prepare: max nonzeros of a row */
 } ps_part_t;
 
 typedef struct ps_params {

@@ -44,7 +44,7 @@ class Csr(ctypes.Structure):
 class Part(ctypes.Structure):
     _fields_ = [("kind", _i32), ("G", _i32), ("n_blocks", _i64), ("block_of", _vp),
                 ("blk_ptr", _vp), ("blk_coords", _vp), ("blk_count", _vp), ("blk_weight", _vp),
-                ("row_blk", _vp), ("row_g", _vp), ("spos", _vp), ("max_slots", _i32)]
+                ("row_blk", _vp), ("row_g", _vp), ("spos", _vp), ("max_slots", _i32), ("max_row_nnz", _i32)]
 
 
 class Params(ctypes.Structure):

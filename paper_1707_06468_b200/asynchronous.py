@@ -32,7 +32,7 @@ class AsyncConfig(SolverConfig):
     counter_batch: int = 100
     warps: int = None           # resident warps (None: library default grid) when threads > 1
     warps_per_cta: int = 0      # 0: library default
-    contention: float = 3.0     # c of gamma_j = gamma * min(1, c * D_j / tau); 0 = plain gamma
+    contention: float = 2.0     # c of gamma_j = gamma * min(1, c * D_j / tau); 0 = plain gamma
 
     def __post_init__(self):
         super().__post_init__()
@@ -92,7 +92,16 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
         trace.append(it, n, obj, time.perf_counter() - start, distance=dist, threads=config.threads)
 
     checkpoint(0)
-    done = 0
+    if not single and not track:
+        # device-pipelined monitor: x snapshots + objectives on a side stream
+        its, objs, secs = dp.run_async_checkpointed(total, every, gamma, seed=config.seed, ctas=ctas,
+                                                    warps_per_cta=wpc, contention=config.contention)
+        t0 = trace.wall_seconds[0]
+        for it, ob, sc in zip(its, objs, secs):
+            trace.append(it, n, ob, t0 + sc, threads=config.threads)
+        done = total
+    else:
+        done = 0
     while done < total:
         nxt = min(total, done + every)
         if single:

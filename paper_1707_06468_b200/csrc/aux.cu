@@ -279,6 +279,7 @@ extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, p
     stats->max_row_nnz = hi32[0];
     stats->max_slots = part->kind == PS_PART_SINGLETON ? hi32[0] : hi32[1];
     part->max_slots = stats->max_slots;
+    part->max_row_nnz = stats->max_row_nnz;
     return PS_OK;
 }
 
@@ -299,6 +300,24 @@ __global__ void __launch_bounds__(256) k_loss_sum(const void *row_ptr, const int
         for (int64_t e = lo + lane; e < hi; e += 32) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
         z = warp_sum(z);
         if (lane == 0) acc += loss_value(loss, z, rvx<VT>(y, i));
+    }
+    block_sum_store(acc, parts);
+}
+
+// thread per row (rows of <= 64 nonzeros): the row's gathers are independent
+// loads in flight together; one loss evaluation per thread.
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(256) k_loss_sum_t(const void *row_ptr, const int32_t *col, const void *val,
+                                                    const void *y, int64_t n, int loss, const double *x, int xs,
+                                                    double *parts)
+{
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        double z = 0.0;
+#pragma unroll 8
+        for (int64_t e = lo; e < hi; e++) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+        acc += loss_value(loss, z, rvx<VT>(y, i));
     }
     block_sum_store(acc, parts);
 }
@@ -365,7 +384,12 @@ extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps
     double *sums = parts + 3 * G1;
     int64_t n = csr->n_rows, p = csr->n_cols;
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (f64 && i64) k_loss_sum<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    if (part->max_row_nnz > 0 && part->max_row_nnz <= 64) {  // short rows: thread per row
+        if (f64 && i64) k_loss_sum_t<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+        else if (f64) k_loss_sum_t<double, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+        else if (i64) k_loss_sum_t<float, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+        else k_loss_sum_t<float, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
+    } else if (f64 && i64) k_loss_sum<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
     else if (f64) k_loss_sum<double, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
     else if (i64) k_loss_sum<float, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
     else k_loss_sum<float, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);

@@ -64,7 +64,8 @@ struct KArgs {
     int32_t H;          // 0 = off
     int32_t period;     // CTA updates between flushes of the pending deltas
     int32_t hot_doubles;  // shared doubles used by the staging area
-    int32_t hot_shift;    // hot slot r is stored at coordinate r << hot_shift
+    int32_t hot_shift;    // hot unit r is stored at unit index r << hot_shift
+    int32_t hot_unit;     // coordinates per hot unit (1: columns, G: contiguous blocks)
     uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
     int32_t diag;         // diagnostics: bit5 hot abar credit direct to L2, bit6 hot x commit direct
     // scratch
@@ -173,6 +174,14 @@ constexpr int HOT_PER_LANE = 32;  // H <= 1024 (dirty bitmask: one 32-bit word p
 constexpr int HOT_MAX = 32 * HOT_PER_LANE;
 constexpr int HOT_TIER0 = 128;  // slots refreshed on every flush
 
+// global coordinate of hot slot s: unit s / U stored at unit (s / U) << hot_shift
+__device__ __forceinline__ int64_t hot_coord(const KArgs &a, int s)
+{
+    if (a.hot_unit <= 1) return (int64_t)s << a.hot_shift;
+    int r = s / a.hot_unit, q = s - r * a.hot_unit;
+    return (((int64_t)r << a.hot_shift) * a.hot_unit) + q;
+}
+
 __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
 {
     extern __shared__ double smem_dyn[];  // h.* point into it: use explicit shared addressing
@@ -190,7 +199,7 @@ __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigne
             dx += smem_take(pend + (2 * c) * H + s);
             dab += smem_take(pend + (2 * c + 1) * H + s);
         }
-        double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
+        double *g = a.coord + 4 * hot_coord(a, s);
         if (dx != 0.0) red_add(g, dx);
         if (dab != 0.0) red_add(g + 1, dab);
     }
@@ -205,7 +214,7 @@ __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigne
         int s = lane + 32 * k;
         if (s < H && (k < HOT_TIER0 / 32 || (k & 3) == (int)rot)) {
             unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dyn + 2 * s);
-            const double *src = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            const double *src = a.coord + 4 * hot_coord(a, s);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
         }
     }
@@ -213,6 +222,65 @@ __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigne
 }
 
 __device__ __forceinline__ void hot_async_drain() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Group-lasso flush (sps_group_kernel): hot blocks accumulate the samples'
+// gradient steps (pending x) and a sample count; the flush applies ONE block
+// prox with the summed threshold, prox_{m g D lam ||.||}(x^_B + sum_k -g v_k),
+// and commits its delta -- a mini-batch proximal step whose fixed point is the
+// optimum (-grad_B f in lam d||x_B||).  Per-sample group prox on a stale
+// snapshot rectifies noise (||c + noise|| > ||c||) into a bias; summing first
+// averages the noise against an m-fold threshold.  abar deltas as usual.
+__device__ __noinline__ void hot_flush_group(const KArgs &a, const HotView &h, int *bcnt, int lane, bool refresh)
+{
+    extern __shared__ double smem_dyn[];
+    const int H = h.H, G = a.G, HB = H / G;
+    double *pend = smem_dyn + 3 * H;
+    for (int r = lane; r < HB; r += 32) {
+        // current global (x, abar) of the block: the prox must act on the value
+        // the delta is added to (the snapshot may predate our previous flush)
+        double2 cur[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+            if (q < G) cur[q] = ld_cg2(a.coord + 4 * hot_coord(a, r * G + q));
+        const int m = atomicExch(bcnt + r, 0);
+        double u[16], ss = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            if (q < G) {
+                const int s = r * G + q;
+                double st = 0.0;
+#pragma unroll
+                for (int c = 0; c < NCOPY; c++) st += smem_take(pend + (2 * c) * H + s);
+                u[q] = cur[q].x + st;
+                ss += u[q] * u[q];
+            }
+        }
+        double f = 1.0;
+        if (m > 0) {
+            const double d = smem_dyn[2 * H + r * G];
+            const double eff = (double)m * a.gamma * fmin(1.0, a.kappa_hot * d) * d;
+            f = group_factor(sqrt(ss), eff, a.lam2);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            if (q < G) {
+                const int s = r * G + q;
+                const double z = m > 0 ? u[q] * f : u[q];
+                const double dz = z - cur[q].x;
+                double dab = 0.0;
+#pragma unroll
+                for (int c = 0; c < NCOPY; c++) dab += smem_take(pend + (2 * c + 1) * H + s);
+                double *gp = a.coord + 4 * hot_coord(a, s);
+                if (dz != 0.0) red_add(gp, dz);
+                if (dab != 0.0) red_add(gp + 1, dab);
+                if (refresh) {
+                    smem_dyn[2 * s] = z;
+                    smem_dyn[2 * s + 1] = cur[q].y + dab;
+                }
+            }
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // SINGLETON fast path: k <= NCH*32, everything in registers.
@@ -513,7 +581,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
     }
     if (a.H > 0) {
         for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
-            const double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            const double *g = a.coord + 4 * hot_coord(a, s);
             reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
             h.d[s] = __ldg(g + 2);
         }
@@ -649,7 +717,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
     if (a.H > 0) {
         for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
-            const double *g = a.coord + 4 * ((int64_t)s << a.hot_shift);
+            const double *g = a.coord + 4 * hot_coord(a, s);
             reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
             h.d[s] = __ldg(g + 2);
         }
@@ -784,6 +852,198 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fast async kernel for group lasso on contiguous blocks of G <= 16
+// coordinates (BASELINE config 5), rows of <= 32 nonzeros.
+//   * the row's distinct blocks (T_i) come from __match_any_sync on col / G,
+//     so rows need not be sorted; block rank = popc of the leader mask;
+//   * the extended support (g blocks x G coordinates) is processed in passes
+//     of 32/G blocks, G lanes per block; x^, abar^, D and the row values per
+//     ext slot are staged in per-warp shared memory between the margin pass
+//     and the prox pass (one read of x^ per coordinate, as worker_iteration);
+//   * block norms by segmented shuffle over the G lanes (penalties.py:103-108);
+//   * hot blocks (all G coordinates) staged per CTA exactly like hot columns.
+template <typename VT, typename PT, int LOSS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
+{
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int nwib = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * nwib + wib;
+    const int G = a.G;
+    const int bpc = 32 / G;
+    HotView h = hot_view(smem_dyn, a.H);
+    unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
+    double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
+    const int HB = a.H / max(G, 1);
+    int *bcnt = reinterpret_cast<int *>(smem_dyn + a.hot_doubles + 17);
+    const int hdr = a.H > 0 ? a.hot_doubles + 17 + (HB + 1) / 2 : 0;
+    // per-warp staging: row value / x^ / abar^ / D per ext slot (32 * G each)
+    double *wa = smem_dyn + hdr + (int64_t)wib * (4 * 32 * G);
+    double *wx = wa + 32 * G, *wab = wx + 32 * G, *wd = wab + 32 * G;
+    if (a.H > 0) {
+        for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
+            const double *g = a.coord + 4 * hot_coord(a, s);
+            reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
+            h.d[s] = __ldg(g + 2);
+        }
+        for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
+        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
+        for (int r = threadIdx.x; r < HB; r += blockDim.x) bcnt[r] = 0;
+        __syncthreads();
+    }
+    const int64_t nwarps = (int64_t)gridDim.x * nwib;
+    const int64_t q0 = a.count / nwarps, rr = a.count % nwarps;
+    uint64_t slot = (uint64_t)(gw * q0 + min(gw, rr));
+    const uint64_t slot_end = slot + (uint64_t)(q0 + (gw < rr ? 1 : 0));
+    const int S = 1 << a.hot_shift;
+    const int hbl = (a.H / max(G, 1)) * S;  // hot block indices are multiples of S below this
+    const double inv_n = 1.0 / a.n_d;
+    int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, nwib) : 0;
+    const int qd = lane % G, tb = lane / G;
+
+    if (slot < slot_end) {
+        RowRegs<VT> cur = fetch_row<VT, PT>(a, sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n), lane);
+        while (true) {
+            const int col = cur.col;
+            const bool act = col >= 0;
+            const int blk = act ? col / G : -1 - lane;
+            const unsigned peers = __match_any_sync(FULL, blk);
+            const int lead = __ffs(peers) - 1;
+            const unsigned leaders = __ballot_sync(FULL, act && lead == lane);
+            const int g = __popc(leaders);
+            const int myrank = __popc(leaders & ((1u << lead) - 1u));
+            double old = 0.0;
+            if (lane == 0) old = ld_cg(a.alpha + cur.i);
+            // row values into their ext slots
+            for (int s2 = lane; s2 < g * G; s2 += 32) wa[s2] = 0.0;
+            __syncwarp();
+            const double cval = widen(cur.val);
+            if (act) wa[myrank * G + (col - blk * G)] = cval;
+            __syncwarp();
+            // ---- pass 1: gather x^, abar^, D on T_i; partial margin
+            double part = 0.0;
+            for (int t0 = 0; t0 < g; t0 += bpc) {
+                const int t = t0 + tb;
+                const bool on = tb < bpc && t < g;
+                const int src = on ? (int)__fns(leaders, 0, t + 1) : 0;
+                const int B = __shfl_sync(FULL, blk, src);
+                if (on) {
+                    const int s2 = t * G + qd;
+                    const int64_t c = (int64_t)B * G + qd;
+                    double xh, ab, d;
+                    if (B < hbl && (B & (S - 1)) == 0) {
+                        const int hs = (B / S) * G + qd;
+                        double2 v = reinterpret_cast<const double2 *>(h.xab)[hs];
+                        xh = v.x;
+                        ab = v.y;
+                        d = h.d[hs];
+                    } else {
+                        double2 v = ld_cg2(a.coord + 4 * c);
+                        xh = v.x;
+                        ab = v.y;
+                        d = __ldg(a.coord + 4 * c + 2);
+                    }
+                    wx[s2] = xh;
+                    wab[s2] = ab;
+                    wd[s2] = d;
+                    part += wa[s2] * xh;
+                }
+            }
+            // ---- prefetch the next sample's row
+            const bool more = slot + 1 < slot_end;
+            slot++;
+            int64_t ni = more ? sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n) : cur.i;
+            int64_t nlo = rp<PT>(a.row_ptr, ni);
+            int nk = more ? (int)(rp<PT>(a.row_ptr, ni + 1) - nlo) : 0;
+            const double margin = warp_sum(part);
+            old = __shfl_sync(FULL, old, 0);
+            const double nw = loss_deriv(LOSS, margin, widen(cur.y));
+            const double ds = nw - old;
+            RowRegs<VT> nxt;
+            nxt.i = ni;
+            nxt.k = nk;
+            nxt.col = -1;
+            nxt.val = VT(0);
+            if (lane < nk) {
+                nxt.col = __ldg(a.col + nlo + lane);
+                nxt.val = __ldg(reinterpret_cast<const VT *>(a.val) + nlo + lane);
+            }
+            nxt.y = more ? __ldg(reinterpret_cast<const VT *>(a.y) + ni) : VT(0);
+            __syncwarp();
+            // ---- pass 2: u, block norms, group shrinkage, commit x on T_i
+            for (int t0 = 0; t0 < g; t0 += bpc) {
+                const int t = t0 + tb;
+                const bool on = tb < bpc && t < g;
+                const int src = on ? (int)__fns(leaders, 0, t + 1) : 0;
+                const int B = __shfl_sync(FULL, blk, src);
+                const int s2 = t * G + qd;
+                double xh = 0.0, u = 0.0, d = 0.0;
+                const bool hot = B < hbl && (B & (S - 1)) == 0;
+                if (on) {
+                    xh = wx[s2];
+                    d = wd[s2];
+                    const double gB = a.gamma * fmin(1.0, (hot ? a.kappa_hot : a.kappa) * d);
+                    double v = d * (wab[s2] + a.lambda1 * xh);
+                    v += ds * wa[s2];
+                    u = xh - gB * v;
+                }
+                double sq = u * u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    double r = __shfl_down_sync(FULL, sq, o);
+                    if (qd + o < G && lane + o < 32) sq += r;
+                }
+                const double ss = __shfl_sync(FULL, sq, lane - qd);
+                if (on) {
+                    if (hot) {  // accumulate the gradient step; block prox at flush
+                        const int hs = (B / S) * G + qd;
+                        atomicAdd(px + hs, u - xh);
+                        if (qd == 0) atomicAdd(bcnt + B / S, 1);
+                    } else {
+                        const double gB = a.gamma * fmin(1.0, a.kappa * d);
+                        const double f = group_factor(sqrt(ss), gB * d, a.lam2);
+                        red_add(a.coord + 4 * ((int64_t)B * G + qd), u * f - xh);
+                    }
+                }
+            }
+            // ---- alpha swap, abar credit on S_i
+            double rep = 0.0;
+            if (lane == 0) rep = atomic_exch(a.alpha + cur.i, nw);
+            rep = __shfl_sync(FULL, rep, 0);
+            const double tt = (nw - rep) * inv_n;
+            if (act) {
+                const bool hot = blk < hbl && (blk & (S - 1)) == 0;
+                if (hot) {
+                    const int hs = (blk / S) * G + (col - blk * G);
+                    atomicAdd(pab + hs, tt * cval);
+                } else {
+                    red_add(a.coord + 4 * (int64_t)col + 1, tt * cval);
+                }
+            }
+            if (a.H > 0 && --until_flush == 0) {
+                hot_flush_group(a, h, bcnt, lane, true);
+                until_flush = a.period;
+            }
+            __syncwarp();
+            if (!more) break;
+            cur = nxt;
+        }
+    }
+    if (lane == 0) {
+        int64_t mine = q0 + (gw < rr ? 1 : 0);
+        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
+    }
+    if (a.H > 0) {
+        hot_async_drain();
+        __syncthreads();
+        if (wib == 0) hot_flush_group(a, h, bcnt, lane, false);
+        hot_async_drain();
+    }
+}
+
 }  // namespace ps
 
 using namespace ps;
@@ -830,6 +1090,20 @@ template <typename VT, typename PT> static void *kernel_ptr_fast(int loss, int p
     if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, FAST_T>;
     return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, FAST_T>;
 }
+constexpr int GROUP_T = 512;
+template <typename VT, typename PT> static void *kernel_ptr_group(int loss)
+{
+    if (loss == PS_LOSS_LOGISTIC) return (void *)sps_group_kernel<VT, PT, PS_LOSS_LOGISTIC, GROUP_T>;
+    return (void *)sps_group_kernel<VT, PT, PS_LOSS_SQUARED, GROUP_T>;
+}
+static void *pick_group(const ps_csr_t *csr, int loss)
+{
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) return kernel_ptr_group<double, long long>(loss);
+    if (f64) return kernel_ptr_group<double, int>(loss);
+    if (i64) return kernel_ptr_group<float, long long>(loss);
+    return kernel_ptr_group<float, int>(loss);
+}
 static void *pick_fast(const ps_csr_t *csr, int loss, int pen)
 {
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
@@ -873,31 +1147,57 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
                          const ps_params_t *prm = nullptr)
 {
     const bool det = sched->samples != nullptr;
-    L->H = (!det && part->kind == PS_PART_SINGLETON) ? std::min(HOT_MAX, std::max(0, (int)sched->hot_cols)) : 0;
-    L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // default: singleton rows of <= 32 nonzeros run one 24-warp CTA per SM (fewest
-    // hot-flush agents, full register budget); everything else 8-warp CTAs
+    const bool diag_generic = (sched->flags & 16) != 0;
+    const int pen = prm ? prm->penalty : PS_PEN_L1;
+    // group-lasso fast kernel: contiguous blocks of G <= 16, rows <= 32 nonzeros
+    const bool group_fast = !det && !diag_generic && part->kind == PS_PART_CONTIG && part->G <= 16 &&
+                            part->max_row_nnz <= 32 && pen == PS_PEN_GROUP && sched->batch <= 0;
+    // singleton rows of <= 32 nonzeros: one 24-warp CTA per SM (fewest hot-flush
+    // agents, full register budget); everything else 8-warp CTAs
     const bool can_big = part->kind == PS_PART_SINGLETON && part->max_slots <= 32;
-    int wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : (can_big ? 24 : 8));
-    bool big = can_big && wpc > 8;
-    L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
-    L->kernel = pick_kernel(csr, part->kind, big);
-    // the pipelined fast kernel: static split, 768-thread CTAs (flags bit 4 forces the generic one)
-    L->fast = !det && can_big && wpc == FAST_T / 32 && sched->batch <= 0 && !(sched->flags & 16);
-    if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, prm ? prm->penalty : PS_PEN_L1);
-    L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
-    L->smem_flag = 0;
-    L->stride = L->M = L->GB = 0;
-    L->gscratch_bytes = 0;
-    if (needs_scratch(csr, part, big)) {
-        L->stride = scratch_layout(csr, part, &L->M, &L->GB);
-        size_t per_cta = (size_t)L->stride * 8 * wpc;
-        if (per_cta + L->smem <= 96 * 1024) {
-            L->smem_flag = 1;
-            L->smem += per_cta;
+    L->H = 0;
+    if (!det && (part->kind == PS_PART_SINGLETON || group_fast))
+        L->H = std::min(HOT_MAX, std::max(0, (int)sched->hot_cols));
+    int wpc;
+    L->fast = false;
+    if (group_fast) {
+        wpc = GROUP_T / 32;
+        const size_t warp_stage = (size_t)wpc * 4 * 32 * part->G * 8;
+        // keep the CTA within the shared-memory budget: shrink the hot set (whole blocks)
+        L->H -= L->H % part->G;  // whole blocks
+        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17 + L->H / part->G) * 8 > 220 * 1024)
+            L->H -= part->G;
+        L->kernel = pick_group(csr, prm ? prm->loss : PS_LOSS_LOGISTIC);
+        L->wpc = wpc;
+        L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
+        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17 + (L->H / part->G + 1) / 2) * 8 : 0);
+        L->smem_flag = 0;
+        L->stride = L->M = L->GB = 0;
+        L->gscratch_bytes = 0;
+        L->fast = true;
+    } else {
+        L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
+        wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : (can_big ? 24 : 8));
+        bool big = can_big && wpc > 8;
+        L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
+        L->kernel = pick_kernel(csr, part->kind, big);
+        // the pipelined fast kernel: static split, 768-thread CTAs (flags bit 4 forces the generic one)
+        L->fast = !det && can_big && wpc == FAST_T / 32 && sched->batch <= 0 && !diag_generic;
+        if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen);
+        L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
+        L->smem_flag = 0;
+        L->stride = L->M = L->GB = 0;
+        L->gscratch_bytes = 0;
+        if (needs_scratch(csr, part, big)) {
+            L->stride = scratch_layout(csr, part, &L->M, &L->GB);
+            size_t per_cta = (size_t)L->stride * 8 * wpc;
+            if (per_cta + L->smem <= 96 * 1024) {
+                L->smem_flag = 1;
+                L->smem += per_cta;
+            }
         }
     }
     if (L->smem > 48 * 1024) {
@@ -987,6 +1287,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     a.H = L.H;
     a.hot_doubles = L.hot_doubles;
     a.hot_shift = std::max(0, (int)sched->hot_shift);
+    a.hot_unit = part->kind == PS_PART_CONTIG ? part->G : 1;
     a.scramble = 0;
     a.diag = sched->flags;
     if (sched->flags & 4) {  // diagnostics: permute the slot order within the call

@@ -95,7 +95,8 @@ class DeviceProblem:
             self.H, self.hot_shift, self.perm, self.perm_np, self.p_dev = 0, 0, None, None, self.p
             self.hot_unit = 1 if self.part_kind == "singleton" else int(self.part.G)
             if self.part_kind in ("singleton", "contiguous") and hot_max > 0 and self.n >= hot_min_rows:
-                units = hot_max if self.hot_unit == 1 else max(1, hot_max // self.hot_unit)
+                # hot_max counts staged coordinates: 256 columns, or ~1024 coordinates of whole blocks
+                units = hot_max if self.hot_unit == 1 else max(1, (4 * hot_max) // self.hot_unit)
                 self._hot_layout(int(units), float(hot_min_frac), int(hot_stride))
             # ---- state
             self.coord = torch.zeros((self.p_dev, 4), dtype=torch.float64, device=dev)
@@ -250,19 +251,62 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self._keep = s
 
-    def run_async(self, count, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=3.0, hot=True,
+    def run_async(self, count, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=2.0, hot=None,
                   hot_period=0, flags=0, stream=None):
         """`count` lock-free updates (asynchronous.py:131-210), continuing the
         sampler stream where the previous call stopped.  ``contention`` = c of
         the per-coordinate step gamma_j = gamma min(1, c D_j / tau) (0: plain
         gamma)."""
-        self.counter.zero_()
+        with self.torch.cuda.stream(stream if stream is not None else self.torch.cuda.current_stream(self.device)):
+            self.counter.zero_()
+        if hot is None:  # shared-memory staging pays for hot columns; for hot blocks the strided layout suffices
+            hot = self.part_kind == "singleton"
         sched = self._sched(count, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta,
                             contention=contention, hot=hot, hot_period=hot_period, flags=flags)
         scr = self._scratch_for(sched)
         _lib.check(_lib.load().ps_run(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self.slot_base += int(count)
+
+    def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, **kw):
+        """`total` async updates in segments of `every`; after each segment x is
+        snapshotted on the device and the objective of the snapshot is evaluated
+        on a side stream while the next segment runs (the reference's monitor,
+        asynchronous.py:187-198, without host round trips).  Returns
+        (iterations, objectives, seconds) with times from device events,
+        measured from the first launch to each checkpoint's objective."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        side = self._side
+        nseg = -(-int(total) // int(every))
+        snaps = [torch.empty(self.p_dev, dtype=torch.float64, device=self.device) for _ in range(min(ring, nseg))]
+        outs = torch.zeros((nseg, 4), dtype=torch.float64, device=self.device)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev_obj = [torch.cuda.Event(enable_timing=True) for _ in range(nseg)]
+        ev_snap = [torch.cuda.Event() for _ in range(nseg)]
+        L = _lib.load()
+        ev0.record(main)
+        done, its = 0, []
+        for k in range(nseg):
+            cnt = min(int(every), int(total) - done)
+            self.run_async(cnt, gamma, seed=seed, stream=main, **kw)
+            done += cnt
+            its.append(done)
+            buf = snaps[k % len(snaps)]
+            if k >= len(snaps):
+                main.wait_event(ev_obj[k - len(snaps)])  # ring slot free again
+            _lib.check(L.ps_coord_get(self.coord.data_ptr(), self.p_dev, 0, buf.data_ptr(), _lib.stream_ptr(main)))
+            ev_snap[k].record(main)
+            side.wait_event(ev_snap[k])
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 1,
+                                      outs[k].data_ptr(), _lib.stream_ptr(side)))
+            ev_obj[k].record(side)
+        torch.cuda.synchronize(self.device)
+        objs = outs[:, :3].sum(dim=1).cpu().numpy().tolist()
+        secs = [ev0.elapsed_time(e) / 1e3 for e in ev_obj]
+        return its, objs, secs
 
     # ------------------------------------------------------------------
     def objective_parts(self, x_ptr=None, stride=4, stream=None):

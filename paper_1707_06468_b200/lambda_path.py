@@ -79,7 +79,7 @@ def run_path(lambdas, solve, rank=None, world=None):
 
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
-                  mode="async", contention=3.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
+                  mode="async", contention=2.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
     """A ``solve(lam)`` closure over one DeviceProblem (uploaded once)."""
     from .device import DeviceProblem
     from .penalties import GroupL2Penalty, L1Penalty
@@ -102,11 +102,11 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
             dp.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas,
                          warps_per_cta=warps_per_cta)
         parts = dp.objective_parts().cpu().numpy()
-        x = dp.x()
-        out = {"objective": float(parts.sum()), "nnz": int(np.count_nonzero(x)),
-               "norm": float(np.linalg.norm(x)), "updates": epochs * n}
+        xt = dp.field(0)  # device vector; summaries reduced on the device
+        out = {"objective": float(parts.sum()), "nnz": int((xt != 0).sum().item()),
+               "norm": float(dp.torch.linalg.vector_norm(xt).item()), "updates": epochs * n}
         if keep_x:
-            out["x"] = x
+            out["x"] = xt.cpu().numpy()
         return out
 
     solve.problem = dp

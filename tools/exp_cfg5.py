@@ -16,8 +16,17 @@ solve = lp.device_solver(d, loss, part, epochs=int(sys.argv[1]) if len(sys.argv)
 dp = solve.problem
 print(json.dumps({"prep_s": time.time() - t0, "lam_max": lam_max, "delta": dp.delta, "n_dead": dp.n_dead,
                   "max_slots": dp.stats.max_slots, "nblocks": dp.n_blocks}), flush=True)
-for frac in (1.0, 0.1, 0.01, 0.001):
-    torch.cuda.synchronize(); t0 = time.time()
-    r = solve(frac * lam_max)
-    torch.cuda.synchronize(); dt = time.time() - t0
-    print(json.dumps({"lam": frac * lam_max, "Mups": r["updates"] / dt / 1e6, "obj": r["objective"], "nnz": r["nnz"], "s": dt}), flush=True)
+ep = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+gamma = solve.gamma
+for frac, hot in ((1.0, True), (1.0, False), (0.01, True), (0.01, False), (0.001, False)):
+    dp.lam2 = frac * lam_max
+    dp.reset_state()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(ep):
+        dp.run_async(d.n_samples, gamma, seed=1, hot=hot)
+    e.record(); torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    xt = dp.field(0)
+    print(json.dumps({"lam": frac * lam_max, "hot": hot, "Mups": ep * d.n_samples / ms / 1e3, "kernel_ms": ms, "obj": dp.objective(),
+                      "nnz": int((xt != 0).sum().item())}), flush=True)
