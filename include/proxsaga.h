@@ -199,6 +199,19 @@ int ps_coord_get_perm(const double *coord, int64_t p, int32_t field, const int32
 int ps_coord_set_perm(double *coord, int64_t p, int32_t field, const int32_t *perm, const double *in,
                       void *stream);
 
+/* K7 device generator for BASELINE configs 3/4: n rows of
+ * k = k_dense + k_zipf distinct sorted columns — [0, k_dense) in every
+ * row, the rest (k_zipf <= 32, k <= 64) drawn Zipf by inverse CDF (cdf[m], device, increasing to 1)
+ * over [k_dense, k_dense + m) with resample-until-distinct; values 1
+ * (lognormal = 0) or lognormal(0,1), rows l2-normalised.  row_ptr int64[n+1],
+ * col int32[n*k], val fp32[n*k]. */
+int ps_gen_zipf_csr(int64_t n, int32_t k_dense, int32_t k_zipf, const double *cdf, int64_t m,
+                    uint64_t seed, int32_t lognormal, int64_t *row_ptr, int32_t *col, float *val,
+                    void *stream);
+/* labels y_i = sign(a_i . w + noise N(0,1)), sign(0) = +1, for the generated CSR */
+int ps_gen_labels(int64_t n, int32_t k, const int32_t *col, const float *val, const double *w,
+                  double noise, uint64_t seed, float *y, void *stream);
+
 /* _atomics.c primitives, device-scope, on caller buffers (test + tooling):
  *   gather      (_atomics.c:163-209)  out[k] = arr[idx[k]]   (L2-coherent loads)
  *   scatter_add (_atomics.c:212-258)  arr[idx[k]] += d[k]     (atomicAdd f64)

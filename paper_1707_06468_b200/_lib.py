@@ -26,7 +26,7 @@ EXPORTS = (
     "ps_resync_average", "ps_prox", "ps_state_reset", "ps_hot_layout", "ps_coord_get", "ps_coord_set",
     "ps_coord_get_perm", "ps_coord_set_perm", "ps_atomic_gather",
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
-    "ps_atomic_add_repeat",
+    "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels",
 )
 
 _vp = ctypes.c_void_p
@@ -105,6 +105,8 @@ def load():
         "ps_atomic_exchange": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
         "ps_atomic_fetch_add_i64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp]),
         "ps_atomic_add_repeat": (_i32, [_vp, _f64, _i64, _i32, _vp]),
+        "ps_gen_zipf_csr": (_i32, [_i64, _i32, _i32, _vp, _i64, ctypes.c_uint64, _i32, _vp, _vp, _vp, _vp]),
+        "ps_gen_labels": (_i32, [_i64, _i32, _vp, _vp, _vp, _f64, ctypes.c_uint64, _vp, _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -12,7 +12,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -676,6 +678,19 @@ __global__ void k_count_ge(const int32_t *counts, int64_t p, int theta, unsigned
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// append the counts >= lo (candidate hot units) to out[0..*m)
+__global__ void k_collect_ge(const int32_t *counts, int64_t nu, int lo, int32_t *out, unsigned long long *m,
+                             int64_t cap)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nu; j += (int64_t)gridDim.x * blockDim.x) {
+        int c = counts[j];
+        if (c >= lo) {
+            unsigned long long s = atomicAdd(m, 1ull);
+            if ((int64_t)s < cap) out[s] = c;
+        }
+    }
+}
+
 // chunked exclusive scan of hot flags: pass 1 per-CTA sums
 __global__ void k_flag_sums(const int32_t *counts, int64_t p, int theta, int64_t chunk, int64_t *sums)
 {
@@ -859,35 +874,33 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
         else if (i64) k_count_units<long long><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
         else k_count_units<int><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
     }
+    // threshold: the smallest theta >= lo = max(1, ceil(min_frac * n)) with at
+    // most hot_max units at or above it.  Candidates (count >= lo) are compacted
+    // on the device; the host picks the (hot_max+1)-th largest from them.
+    const int lo = std::max(1, (int)std::ceil(min_frac * (double)n));
     unsigned long long *cnt = nullptr;
+    int32_t *cand = nullptr;
+    const int64_t cap = std::min<int64_t>(nu, 1 << 24);
     CK(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long), st), "ps_hot_layout alloc");
-    auto count_ge = [&](int theta, unsigned long long *h) -> int {
-        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "ps_hot_layout memset");
-        k_count_ge<<<grid, 256, 0, st>>>(counts_ws, nu, theta, cnt);
-        CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "ps_hot_layout copy");
-        CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
-        return PS_OK;
-    };
-    // smallest theta >= min_frac*n (and >= 1) with at most hot_max qualifying units
-    int lo = std::max(1, (int)std::ceil(min_frac * (double)n));
-    unsigned long long h = 0;
-    int r = count_ge(lo, &h);
-    if (r) return r;
+    CK(cudaMallocAsync((void **)&cand, sizeof(int32_t) * std::max<int64_t>(cap, 1), st), "ps_hot_layout alloc");
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "ps_hot_layout memset");
+    k_collect_ge<<<grid, 256, 0, st>>>(counts_ws, nu, lo, cand, cnt, cap);
+    unsigned long long m = 0;
+    CK(cudaMemcpyAsync(&m, cnt, sizeof(m), cudaMemcpyDeviceToHost, st), "ps_hot_layout copy");
+    CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
     int theta = lo;
-    if (h > (unsigned long long)hot_max) {
-        int a = lo, b = (int)std::min<int64_t>(n + 1, INT32_MAX);
-        while (b - a > 1) {
-            int mid = a + (b - a) / 2;
-            r = count_ge(mid, &h);
-            if (r) return r;
-            if (h > (unsigned long long)hot_max) a = mid;
-            else b = mid;
-        }
-        theta = b;
+    int H = (int)std::min<unsigned long long>(m, (unsigned long long)cap);
+    if ((int64_t)m > cap) return ps_fail(PS_EINVAL, "too many hot candidates; raise min_frac");
+    if (m > (unsigned long long)hot_max) {
+        std::vector<int32_t> hv(m);
+        CK(cudaMemcpyAsync(hv.data(), cand, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st), "ps_hot_layout copy");
+        CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
+        std::nth_element(hv.begin(), hv.begin() + hot_max, hv.end(), std::greater<int32_t>());
+        theta = hv[hot_max] + 1;  // strictly above the (hot_max+1)-th largest count
+        H = 0;
+        for (int32_t v : hv) H += v >= theta;
     }
-    r = count_ge(theta, &h);
-    if (r) return r;
-    int H = (int)h;
+    CK(cudaFreeAsync(cand, st), "ps_hot_layout free");
     int S = *stride_inout;
     while (S > 1 && (int64_t)S * H > nu) S >>= 1;  // hot units at 0, S, 2S, ... (unit indices)
     const int64_t chunk = 1 << 12;

@@ -51,20 +51,24 @@ class DeviceProblem:
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
                  value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
-                 _labels=None):
+                 _labels=None, _device_csr=None, _shape=None):
         torch = _torch()
         _lib.require_device()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    (device.index if isinstance(device, torch.device) else int(device)))
-        f = data.features if hasattr(data, "features") else data
-        labels = data.labels if _labels is None else _labels
-        self.n, self.p = int(f.n_rows), int(f.n_cols)
+        if _device_csr is not None:
+            f, labels = None, None
+            self.n, self.p, self.nnz = (int(v) for v in _shape)
+        else:
+            f = data.features if hasattr(data, "features") else data
+            labels = data.labels if _labels is None else _labels
+            self.n, self.p = int(f.n_rows), int(f.n_cols)
+            self.nnz = int(f.row_offsets[-1])
         if self.n < 1:
             raise ValueError("dataset is empty")
         if self.p >= 2 ** 31:
             raise ValueError("n_cols must fit int32")
-        self.nnz = int(f.row_offsets[-1])
         self.loss_kind = loss.kind if loss is not None else "squared"
         self.lambda1 = float(loss.lambda1) if loss is not None else 0.0
         if penalty is None:
@@ -73,21 +77,26 @@ class DeviceProblem:
             self.pen_code, self.lam2, self.lo, self.hi = penalty_code(penalty)
         dev = self.device
         with torch.cuda.device(dev):
-            # ---- CSR upload
-            ro = np.asarray(f.row_offsets)
-            self.row_ptr_type = _lib.I32 if self.nnz < 2 ** 31 - 1 else _lib.I64
-            self.row_ptr = torch.from_numpy(np.ascontiguousarray(
-                ro, dtype=np.int32 if self.row_ptr_type == _lib.I32 else np.int64)).to(dev)
-            self.col = torch.from_numpy(np.ascontiguousarray(f.col_indices, dtype=np.int32)).to(dev)
-            vals = np.asarray(f.values)
-            if value_dtype == "auto":
-                use32 = _f32_exact(vals) and _f32_exact(labels)
+            if _device_csr is not None:  # already on the device (K7 generator)
+                self.row_ptr, self.col, self.val, self.y = _device_csr
+                self.row_ptr_type = _lib.I32 if self.row_ptr.dtype == torch.int32 else _lib.I64
+                self.value_type = _lib.F32 if self.val.dtype == torch.float32 else _lib.F64
             else:
-                use32 = np.dtype(value_dtype) == np.float32
-            self.value_type = _lib.F32 if use32 else _lib.F64
-            vdt = np.float32 if use32 else np.float64
-            self.val = torch.from_numpy(np.ascontiguousarray(vals, dtype=vdt)).to(dev)
-            self.y = torch.from_numpy(np.ascontiguousarray(labels, dtype=vdt)).to(dev)
+                # ---- CSR upload
+                ro = np.asarray(f.row_offsets)
+                self.row_ptr_type = _lib.I32 if self.nnz < 2 ** 31 - 1 else _lib.I64
+                self.row_ptr = torch.from_numpy(np.ascontiguousarray(
+                    ro, dtype=np.int32 if self.row_ptr_type == _lib.I32 else np.int64)).to(dev)
+                self.col = torch.from_numpy(np.ascontiguousarray(f.col_indices, dtype=np.int32)).to(dev)
+                vals = np.asarray(f.values)
+                if value_dtype == "auto":
+                    use32 = _f32_exact(vals) and _f32_exact(labels)
+                else:
+                    use32 = np.dtype(value_dtype) == np.float32
+                self.value_type = _lib.F32 if use32 else _lib.F64
+                vdt = np.float32 if use32 else np.float64
+                self.val = torch.from_numpy(np.ascontiguousarray(vals, dtype=vdt)).to(dev)
+                self.y = torch.from_numpy(np.ascontiguousarray(labels, dtype=vdt)).to(dev)
             self.csr = _lib.Csr(self.n, self.p, self.nnz, self.row_ptr.data_ptr(), self.col.data_ptr(),
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
             # ---- partition (+ hot-column renumbering for singleton layouts)
@@ -116,6 +125,14 @@ class DeviceProblem:
         self._scratch = None
         self._out = torch.zeros(4, dtype=torch.float64, device=dev)
         self._grad = None
+
+    @classmethod
+    def from_device_csr(cls, row_ptr, col, val, y, p, loss, penalty, partition=None, device=None, **kw):
+        """A problem whose CSR already lives on the device (torch tensors:
+        row_ptr int32/int64[n+1], col int32[nnz], val / y fp32 or fp64)."""
+        n = int(row_ptr.numel()) - 1
+        return cls(None, loss, penalty, partition, device=device, drop_dead_blocks=True,
+                   _device_csr=(row_ptr, col, val, y), _shape=(n, p, int(col.numel())), **kw)
 
     @classmethod
     def for_index(cls, features, partition, device=None):

@@ -222,3 +222,69 @@ def config5(seed=0, n=100_000, p=10_000_000, group=10):
 
 def baseline_config(k, seed=0, **kw):
     return {1: config1, 2: config2, 5: config5}[k](seed=seed, **kw)
+
+
+# ---------------------------------------------------------------------------
+# Configs 3 and 4 at full size: generated on the device (K7, csrc/gen.cu)
+
+def _zipf_cdf(m, s):
+    w = np.arange(1, m + 1, dtype=np.float64) ** (-s)
+    c = np.cumsum(w)
+    c /= c[-1]
+    return c
+
+
+def device_zipf_problem(n, p, k_dense, k_zipf, s, n_planted, lam2, lognormal, seed=0, device=None, noise=0.1,
+                        **problem_kw):
+    """Generate a logistic l1 problem on the device and wrap it in a
+    DeviceProblem (lambda1 = 1/n, gamma rule 1/2L as configs 2-5)."""
+    import torch
+
+    from . import _lib
+    from .device import DeviceProblem
+
+    _lib.require_device()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+    k = k_dense + k_zipf
+    nnz = n * k
+    m = p - k_dense
+    cdf = torch.from_numpy(_zipf_cdf(m, s)).to(dev)
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz, dtype=torch.float32, device=dev)
+    L = _lib.load()
+    _lib.check(L.ps_gen_zipf_csr(n, k_dense, k_zipf, cdf.data_ptr(), m, seed, int(lognormal), row_ptr.data_ptr(),
+                                 col.data_ptr(), val.data_ptr(), _lib.stream_ptr()))
+    del cdf
+    rng = np.random.default_rng(seed)
+    w = np.zeros(p)
+    sup = rng.choice(p, size=min(n_planted, p), replace=False)
+    w[sup] = rng.standard_normal(len(sup))
+    wt = torch.from_numpy(w).to(dev)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    _lib.check(L.ps_gen_labels(n, k, col.data_ptr(), val.data_ptr(), wt.data_ptr(), noise, seed + 1, y.data_ptr(),
+                               _lib.stream_ptr()))
+    del wt
+    if nnz < 2 ** 31 - 1:
+        row_ptr = row_ptr.to(torch.int32)
+    loss = Loss(LOGISTIC, 1.0 / n)
+    pen = L1Penalty(lam2)
+    dp = DeviceProblem.from_device_csr(row_ptr, col, val, y, p, loss, pen, None, device=dev, **problem_kw)
+    return dict(problem=dp, loss=loss, penalty=pen, step="1/2L", k=k)
+
+
+def config3(seed=0, n=20_000_000, p=30_000_000, **kw):
+    """l1-logistic, n=2e7 x p=3e7, 30 distinct Zipf(1.2) columns per row, binary
+    values row-normalised, planted w* with 10k nonzeros, lambda=1e-7, 10 epochs."""
+    d = device_zipf_problem(n, p, 0, 30, 1.2, 10_000, 1e-7, False, seed=seed, **kw)
+    d.update(epochs=10, name=f"cfg3-l1logistic-{n}x{p}-zipf1.2")
+    return d
+
+
+def config4(seed=0, n=45_000_000, p=1_000_000, **kw):
+    """l1-logistic, n=4.5e7 x p=1e6, 13 dense columns + 22 Zipf(1.05) per row,
+    lognormal(0,1) values row-normalised, planted w* with 2k nonzeros,
+    lambda=1e-6, 5 epochs."""
+    d = device_zipf_problem(n, p, 13, 22, 1.05, 2_000, 1e-6, True, seed=seed, **kw)
+    d.update(epochs=5, name=f"cfg4-l1logistic-{n}x{p}-dense13+zipf1.05")
+    return d
