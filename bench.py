@@ -192,6 +192,40 @@ def lambda_path_bench(rank, world, epochs):
     return res
 
 
+def big_config_bench(which, peak):
+    """Full-size BASELINE config 3 / 4, generated on the device (K7): one
+    launch of the config's epochs from x0 = 0, device-timed; HBM roofline from
+    SURVEY §8d bytes/update (the working set does not fit L2 here)."""
+    import torch
+
+    import paper_1707_06468_b200 as pb
+    from paper_1707_06468_b200 import problems
+
+    c = problems.config3() if which == 3 else problems.config4()
+    dp = c["problem"]
+    gamma = pb.resolve_step_size(c["step"], dp.L, dp.n, c["loss"].lambda1)
+    dp.run_async(dp.n // 10, gamma, seed=1)  # warm-up
+    dp.reset_state()
+    f0 = dp.objective()
+    total = c["epochs"] * dp.n
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    dp.run_async(total, gamma, seed=2)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    f1 = dp.objective()
+    bpu = dp.bytes_per_update()
+    ups = total / (ms / 1e3)
+    out = {"workload": c["name"] + f", {c['epochs']} async epochs from x0=0 in one launch, device-generated (K7)",
+           "n": dp.n, "p": dp.p, "nnz": dp.nnz, "value": ups, "unit": UNIT, "kernel_ms": ms,
+           "bytes_per_update": bpu, "achieved_GBps": bpu * ups / 1e9, "roofline_frac": bpu * ups / 1e9 / peak,
+           "objective_start": f0, "objective_end": f1, "hot_columns": dp.H}
+    del dp, c
+    torch.cuda.empty_cache()
+    return out
+
+
 def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
     """Solve from zero with an objective checkpoint every epoch.  Checkpoints
     are pipelined on the device (DeviceProblem.run_async_checkpointed: x
@@ -228,6 +262,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-path", action="store_true")
+    ap.add_argument("--no-big", action="store_true")
     ap.add_argument("--path-epochs", type=int, default=30)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -357,6 +392,11 @@ def main():
                  "value": upd / (float(t.item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t.item()),
                  "n_gpus": world, "algorithmic_bytes_per_update_est": lp_local["bytes_per_update_est"]}
 
+    big = {}
+    if world == 1 and not args.no_big:
+        for which in (3, 4):
+            big[f"config{which}"] = big_config_bench(which, peak)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -383,6 +423,8 @@ def main():
             "gpu_launches": 2 * args.steps,
             "cpu_baseline": cpu,
             "lambda_path": lpath,
+            "config3": big.get("config3"),
+            "config4": big.get("config4"),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
