@@ -109,11 +109,18 @@ typedef struct ps_sched {
                                 tau = effective delay in updates (async only; the fixed point is
                                 unchanged); 0 = plain gamma (the reference's step) */
     int32_t hot_period;      /* CTA updates between hot flushes (0 = default) */
-    int32_t flags;           /* bit0: hot reads add this CTA's pending deltas; bit1: hot reads
-                                from L2 instead of the snapshot (diagnostics) */
+    int32_t flags;           /* PS_FLAG_* below (0 = defaults) */
     int32_t hot_shift;       /* log2 of the hot-record stride of ps_hot_layout */
     int32_t reserved;
 } ps_sched_t;
+
+/* ps_sched_t.flags (async only; diagnostics except where noted) */
+#define PS_FLAG_SCRAMBLE 4        /* permute the slot order within the call */
+#define PS_FLAG_GENERIC 16        /* force the generic kernel (no pipelined fast path) */
+#define PS_FLAG_DELTA_ZERO 32     /* commit prox-zeroed coordinates as the delta -x_hat, the
+                                     reference's literal scatter_add (asynchronous.py:105-107);
+                                     default: store 0 */
+/* bits 8..15: extra divisor of the staged columns' contention scale */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);

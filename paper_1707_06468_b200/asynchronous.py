@@ -32,7 +32,7 @@ class AsyncConfig(SolverConfig):
     counter_batch: int = 100
     warps: int = None           # resident warps (None: library default grid) when threads > 1
     warps_per_cta: int = 0      # 0: library default
-    contention: float = 2.0     # c of gamma_j = gamma * min(1, c * D_j / tau); 0 = plain gamma
+    contention: float = 4.0     # c of gamma_j = gamma * min(1, c * D_j / tau); 0 = plain gamma
 
     def __post_init__(self):
         super().__post_init__()

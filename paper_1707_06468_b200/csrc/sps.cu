@@ -116,6 +116,7 @@ __device__ __forceinline__ double step_of(const KArgs &a, double d)
 __device__ __forceinline__ void commit_x(const KArgs &a, int64_t c, double xh, double z)
 {
     if (a.det) a.coord[4 * c] = xh + (z - xh);
+    else if (z == 0.0 && !(a.diag & PS_FLAG_DELTA_ZERO)) atomic_exch(a.coord + 4 * c, 0.0);  // see store_zero
     else red_add(a.coord + 4 * c, z - xh);
 }
 
@@ -163,6 +164,12 @@ __device__ __forceinline__ void mark_dirty(unsigned *dirty, int slot)
 __device__ __forceinline__ double smem_take(double *p)
 {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
+}
+// discard this CTA's pending x delta of a staged slot (its coordinate is being stored)
+__device__ __forceinline__ void drop_pending_x(const HotView &h, int s)
+{
+#pragma unroll
+    for (int c = 0; c < NCOPY; c++) atomicExch(reinterpret_cast<unsigned long long *>(h.pend + (2 * c) * h.H + s), 0ull);
 }
 
 // flush this CTA's pending deltas to global, then refresh the snapshot.
@@ -330,10 +337,11 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
             double g = slot[c] >= 0 ? a.gamma * fmin(1.0, a.kappa_hot * dr[c]) : step_of(a, dr[c]);
             double u = xr[c] - g * v;
             double z = prox_sep(a.pen, u, g * dr[c], a.lam2, a.lo, a.hi);
-            if (slot[c] >= 0) {
+            if (slot[c] >= 0 && (z != 0.0 || (a.diag & PS_FLAG_DELTA_ZERO))) {
                 atomicAdd(px + slot[c], z - xr[c]);
                 mark_dirty(dirty, slot[c]);
             } else {
+                if (slot[c] >= 0) drop_pending_x(h, slot[c]);
                 commit_x(a, colr[c], xr[c], z);
             }
         }
@@ -689,22 +697,62 @@ __device__ __forceinline__ RowRegs<VT> fetch_row(const KArgs &a, int64_t i, int 
     return r;
 }
 
-template <int PEN> __device__ __forceinline__ double prox_t(const KArgs &a, double u, double eff)
+template <int PEN>
+__device__ __forceinline__ double prox_t(double u, double eff, double lam2, int pen, double lo, double hi)
 {
     if (PEN == PS_PEN_L1) {
-        double thr = eff * a.lam2;
+        double thr = eff * lam2;
         double m = fmax(fabs(u) - thr, 0.0);
         return u > 0 ? m : (u < 0 ? -m : 0.0);
     }
-    return prox_sep(a.pen, u, eff, a.lam2, a.lo, a.hi);
+    return prox_sep(pen, u, eff, lam2, lo, hi);
 }
 
+// losses.py:73-86 with one division: et = exp(-|t|); sig = (t > 0 ? 1 : et) / (1 + et)
+// -- the same two expressions as the reference's branches, no divergence.
 template <int LOSS> __device__ __forceinline__ double deriv_t(double z, double b)
 {
-    return loss_deriv(LOSS, z, b);
+    if (LOSS == PS_LOSS_LOGISTIC) {
+        double t = -b * z;
+        double et = exp(-fabs(t));
+        double sig = (t > 0 ? 1.0 : et) / (1.0 + et);
+        return -b * sig;
+    }
+    return z - b;
 }
 
-template <typename VT, typename PT, int LOSS, int PEN, int MAXT>
+// per-lane state of one update: NC nonzeros per lane (rows of <= 32 * NC)
+template <typename VT, int NC> struct Row {
+    int64_t i;
+    int col[NC];
+    VT val[NC];
+    VT y;
+};
+
+template <typename VT, typename PT, int NC>
+__device__ __forceinline__ void fetch_rowc(const KArgs &a, int64_t i, int lane, Row<VT, NC> &r, bool valid)
+{
+    r.i = i;
+    int64_t lo = 0;
+    int k = 0;
+    if (valid) {
+        lo = rp<PT>(a.row_ptr, i);
+        k = (int)(rp<PT>(a.row_ptr, i + 1) - lo);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        const int e = lane + 32 * c;
+        r.col[c] = -1;
+        r.val[c] = VT(0);
+        if (e < k) {
+            r.col[c] = __ldg(a.col + lo + e);
+            r.val[c] = __ldg(reinterpret_cast<const VT *>(a.val) + lo + e);
+        }
+    }
+    r.y = valid ? __ldg(reinterpret_cast<const VT *>(a.y) + i) : VT(0);
+}
+
+template <typename VT, typename PT, int LOSS, int PEN, int NC, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
 {
     extern __shared__ double smem_dyn[];
@@ -725,99 +773,118 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
+    // kernel parameters used in the loop, hoisted
+    double *const coord = a.coord;
+    double *const alpha = a.alpha;
+    const double gamma = a.gamma, lambda1 = a.lambda1, kappa = a.kappa, kappa_hot = a.kappa_hot, lam2 = a.lam2;
+    const double plo = a.lo, phi = a.hi;
+    const int pen = a.pen;
+    const int shift = a.hot_shift;
+    const int hmask = (1 << shift) - 1, hlim = a.H << shift;
+    const uint64_t seed = a.seed, base = a.slot_base, nrows = (uint64_t)a.n;
+    const double inv_n = 1.0 / a.n_d;
+    const bool store_zero = !(a.diag & PS_FLAG_DELTA_ZERO);
     const int64_t nwarps = (int64_t)gridDim.x * nwib;
     const int64_t q = a.count / nwarps, rr = a.count % nwarps;
     uint64_t slot = (uint64_t)(gw * q + min(gw, rr));
     const uint64_t slot_end = slot + (uint64_t)(q + (gw < rr ? 1 : 0));
-    const int hmask = (1 << a.hot_shift) - 1, hlim = a.H << a.hot_shift;
-    const double inv_n = 1.0 / a.n_d;
     int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, nwib) : 0;
 
     // pending abar credit of the previous update
-    int pcol = -1, pslot = -1;
-    double pval = 0.0, pnw = 0.0, prep = 0.0;
-    bool pend_credit = false;
+    int pcol[NC], pslot[NC];
+    double pval[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) pcol[c] = -1;
+    double pnw = 0.0, prep = 0.0;
 
     if (slot < slot_end) {
-        RowRegs<VT> cur = fetch_row<VT, PT>(a, sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n), lane);
+        Row<VT, NC> cur;
+        fetch_rowc<VT, PT, NC>(a, sample_row(seed, base + slot, nrows), lane, cur, true);
         while (true) {
-            // ---- state reads of the current update
-            const int col = cur.col;
-            int sl = -1;
-            double xh = 0.0, ab = 0.0, d = 0.0;
-            if (col >= 0) {
-                if (col < hlim && (col & hmask) == 0) sl = col >> a.hot_shift;
-                if (sl >= 0) {
-                    double2 v = reinterpret_cast<const double2 *>(h.xab)[sl];
-                    xh = v.x;
-                    ab = v.y;
-                    d = h.d[sl];
-                } else {
-                    double2 xa = ld_cg2(a.coord + 4 * (int64_t)col);
-                    xh = xa.x;
-                    ab = xa.y;
-                    d = __ldg(a.coord + 4 * (int64_t)col + 2);
+            // ---- state reads (hot: CTA snapshot in shared memory; cold: one
+            // 16-B L2 read + D through the read-only path)
+            int sl[NC];
+            double xh[NC], ab[NC], d[NC];
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const int col = cur.col[c];
+                sl[c] = (col >= 0 && col < hlim && (col & hmask) == 0) ? (col >> shift) : -1;
+                xh[c] = ab[c] = d[c] = 0.0;
+                if (col >= 0) {
+                    if (sl[c] >= 0) {
+                        double2 v = reinterpret_cast<const double2 *>(h.xab)[sl[c]];
+                        xh[c] = v.x;
+                        ab[c] = v.y;
+                        d[c] = h.d[sl[c]];
+                    } else {
+                        double2 v = ld_cg2(coord + 4 * (int64_t)col);
+                        xh[c] = v.x;
+                        ab[c] = v.y;
+                        d[c] = __ldg(coord + 4 * (int64_t)col + 2);
+                    }
                 }
             }
             double old = 0.0;
-            if (lane == 0) old = ld_cg(a.alpha + cur.i);
+            if (lane == 0) old = ld_cg(alpha + cur.i);
             // ---- abar credit of the previous update (its exchange has returned by now)
-            if (pend_credit) {
-                double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
-                if (pcol >= 0) {
-                    if (pslot >= 0 && !(a.diag & 32)) {
-                        atomicAdd(pab + pslot, t * pval);
-                        mark_dirty(dirty, pslot);
-                    } else {
-                        red_add(a.coord + 4 * (int64_t)pcol + 1, t * pval);
+            {
+                const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    if (pcol[c] >= 0) {
+                        if (pslot[c] >= 0) {
+                            atomicAdd(pab + pslot[c], t * pval[c]);
+                            mark_dirty(dirty, pslot[c]);
+                        } else {
+                            red_add(coord + 4 * (int64_t)pcol[c] + 1, t * pval[c]);
+                        }
                     }
                 }
             }
             // ---- prefetch the next sample's row (independent of the state)
             const bool more = slot + 1 < slot_end;
             slot++;
-            int64_t ni = more ? sample_row(a.seed, a.slot_base + slot, (uint64_t)a.n) : cur.i;
-            int64_t nlo = rp<PT>(a.row_ptr, ni);
-            int nk = more ? (int)(rp<PT>(a.row_ptr, ni + 1) - nlo) : 0;
-            // ---- margin -> derivative -> prox
-            const double cval = widen(cur.val);
-            double margin = warp_sum(col >= 0 ? cval * xh : 0.0);
+            Row<VT, NC> nxt;
+            fetch_rowc<VT, PT, NC>(a, more ? sample_row(seed, base + slot, nrows) : cur.i, lane, nxt, more);
+            // ---- margin -> derivative -> prox -> commit x
+            double part = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; c++) part += widen(cur.val[c]) * xh[c];
+            const double margin = warp_sum(part);
             old = __shfl_sync(FULL, old, 0);
-            double nw = deriv_t<LOSS>(margin, widen(cur.y));
-            double ds = nw - old;
-            // next row's columns / values / label
-            RowRegs<VT> nxt;
-            nxt.i = ni;
-            nxt.k = nk;
-            nxt.col = -1;
-            nxt.val = VT(0);
-            if (lane < nk) {
-                nxt.col = __ldg(a.col + nlo + lane);
-                nxt.val = __ldg(reinterpret_cast<const VT *>(a.val) + nlo + lane);
-            }
-            nxt.y = more ? __ldg(reinterpret_cast<const VT *>(a.y) + ni) : VT(0);
-            if (col >= 0) {
-                double v = d * (ab + a.lambda1 * xh);
-                v += ds * cval;
-                double g = a.gamma * fmin(1.0, (sl >= 0 ? a.kappa_hot : a.kappa) * d);
-                double u = xh - g * v;
-                double z = prox_t<PEN>(a, u, g * d);
-                if (sl >= 0 && !(a.diag & 64)) {
-                    atomicAdd(px + sl, z - xh);
-                    mark_dirty(dirty, sl);
-                } else {
-                    red_add(a.coord + 4 * (int64_t)col, z - xh);
+            const double nw = deriv_t<LOSS>(margin, widen(cur.y));
+            const double ds = nw - old;
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const int col = cur.col[c];
+                if (col >= 0) {
+                    const double cval = widen(cur.val[c]);
+                    double v = d[c] * (ab[c] + lambda1 * xh[c]);
+                    v += ds * cval;
+                    const double g = gamma * fmin(1.0, (sl[c] >= 0 ? kappa_hot : kappa) * d[c]);
+                    const double u = xh[c] - g * v;
+                    const double z = prox_t<PEN>(u, g * d[c], lam2, pen, plo, phi);
+                    if (z == 0.0 && store_zero) {
+                        // the prox zeroed the coordinate: commit it as a store, not as the
+                        // delta -x_hat; drops this CTA's pending delta
+                        if (sl[c] >= 0) drop_pending_x(h, sl[c]);
+                        atomic_exch(coord + 4 * (int64_t)col, 0.0);
+                    } else if (sl[c] >= 0) {
+                        atomicAdd(px + sl[c], z - xh[c]);
+                        mark_dirty(dirty, sl[c]);
+                    } else {
+                        red_add(coord + 4 * (int64_t)col, z - xh[c]);
+                    }
                 }
+                pcol[c] = col;
+                pslot[c] = sl[c];
+                pval[c] = widen(cur.val[c]);
             }
             // ---- alpha_i <-> new (consumed next iteration)
             double rep = 0.0;
-            if (lane == 0) rep = atomic_exch(a.alpha + cur.i, nw);
-            pcol = col;
-            pslot = sl;
-            pval = cval;
+            if (lane == 0) rep = atomic_exch(alpha + cur.i, nw);
             pnw = nw;
             prep = rep;
-            pend_credit = true;
             if (a.H > 0 && --until_flush == 0) {
                 hot_flush(a, h, dirty, lane, true);
                 until_flush = a.period;
@@ -826,13 +893,16 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             cur = nxt;
         }
         // last credit
-        double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
-        if (pcol >= 0) {
-            if (pslot >= 0 && !(a.diag & 32)) {
-                atomicAdd(pab + pslot, t * pval);
-                mark_dirty(dirty, pslot);
-            } else {
-                red_add(a.coord + 4 * (int64_t)pcol + 1, t * pval);
+        const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            if (pcol[c] >= 0) {
+                if (pslot[c] >= 0) {
+                    atomicAdd(pab + pslot[c], t * pval[c]);
+                    mark_dirty(dirty, pslot[c]);
+                } else {
+                    red_add(coord + 4 * (int64_t)pcol[c] + 1, t * pval[c]);
+                }
             }
         }
     }
@@ -851,7 +921,6 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         hot_async_drain();
     }
 }
-
 
 // ---------------------------------------------------------------------------
 // Fast async kernel for group lasso on contiguous blocks of G <= 16
@@ -874,6 +943,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
     const int64_t gw = (int64_t)blockIdx.x * nwib + wib;
     const int G = a.G;
     const int bpc = 32 / G;
+    const bool store_zero = !(a.diag & PS_FLAG_DELTA_ZERO);
     HotView h = hot_view(smem_dyn, a.H);
     unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
@@ -1005,7 +1075,8 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
                     } else {
                         const double gB = a.gamma * fmin(1.0, a.kappa * d);
                         const double f = group_factor(sqrt(ss), gB * d, a.lam2);
-                        red_add(a.coord + 4 * ((int64_t)B * G + qd), u * f - xh);
+                        if (f == 0.0 && store_zero) atomic_exch(a.coord + 4 * ((int64_t)B * G + qd), 0.0);
+                        else red_add(a.coord + 4 * ((int64_t)B * G + qd), u * f - xh);
                     }
                 }
             }
@@ -1081,14 +1152,14 @@ template <typename VT, typename PT> static void *kernel_ptr_big()
     return (void *)sps_kernel<VT, PT, PS_PART_SINGLETON, 1024>;
 }
 constexpr int FAST_T = 768;
-template <typename VT, typename PT> static void *kernel_ptr_fast(int loss, int pen)
+template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int loss, int pen)
 {
     if (loss == PS_LOSS_LOGISTIC) {
-        if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, FAST_T>;
-        return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, FAST_T>;
+        if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, NC, FAST_T>;
+        return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, NC, FAST_T>;
     }
-    if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, FAST_T>;
-    return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, FAST_T>;
+    if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, NC, FAST_T>;
+    return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, NC, FAST_T>;
 }
 constexpr int GROUP_T = 512;
 template <typename VT, typename PT> static void *kernel_ptr_group(int loss)
@@ -1104,13 +1175,19 @@ static void *pick_group(const ps_csr_t *csr, int loss)
     if (i64) return kernel_ptr_group<float, long long>(loss);
     return kernel_ptr_group<float, int>(loss);
 }
-static void *pick_fast(const ps_csr_t *csr, int loss, int pen)
+static void *pick_fast(const ps_csr_t *csr, int loss, int pen, int nc)
 {
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (f64 && i64) return kernel_ptr_fast<double, long long>(loss, pen);
-    if (f64) return kernel_ptr_fast<double, int>(loss, pen);
-    if (i64) return kernel_ptr_fast<float, long long>(loss, pen);
-    return kernel_ptr_fast<float, int>(loss, pen);
+    if (nc == 1) {
+        if (f64 && i64) return kernel_ptr_fast<double, long long, 1>(loss, pen);
+        if (f64) return kernel_ptr_fast<double, int, 1>(loss, pen);
+        if (i64) return kernel_ptr_fast<float, long long, 1>(loss, pen);
+        return kernel_ptr_fast<float, int, 1>(loss, pen);
+    }
+    if (f64 && i64) return kernel_ptr_fast<double, long long, 2>(loss, pen);
+    if (f64) return kernel_ptr_fast<double, int, 2>(loss, pen);
+    if (i64) return kernel_ptr_fast<float, long long, 2>(loss, pen);
+    return kernel_ptr_fast<float, int, 2>(loss, pen);
 }
 
 static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
@@ -1155,9 +1232,11 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     // group-lasso fast kernel: contiguous blocks of G <= 16, rows <= 32 nonzeros
     const bool group_fast = !det && !diag_generic && part->kind == PS_PART_CONTIG && part->G <= 16 &&
                             part->max_row_nnz <= 32 && pen == PS_PEN_GROUP && sched->batch <= 0;
-    // singleton rows of <= 32 nonzeros: one 24-warp CTA per SM (fewest hot-flush
-    // agents, full register budget); everything else 8-warp CTAs
+    // singleton rows of <= 32 (<= 64 for the fast kernel) nonzeros: one 24-warp
+    // CTA per SM (fewest hot-flush agents, full register budget); else 8-warp CTAs
     const bool can_big = part->kind == PS_PART_SINGLETON && part->max_slots <= 32;
+    const bool can_fast = part->kind == PS_PART_SINGLETON && part->max_slots <= 64 && !det && sched->batch <= 0 &&
+                          !diag_generic && (sched->warps_per_cta <= 0 || sched->warps_per_cta == FAST_T / 32);
     L->H = 0;
     if (!det && (part->kind == PS_PART_SINGLETON || group_fast))
         L->H = std::min(HOT_MAX, std::max(0, (int)sched->hot_cols));
@@ -1180,13 +1259,14 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         L->fast = true;
     } else {
         L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
-        wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : (can_big ? 24 : 8));
+        wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : ((can_big || can_fast) ? 24 : 8));
         bool big = can_big && wpc > 8;
-        L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
-        L->kernel = pick_kernel(csr, part->kind, big);
         // the pipelined fast kernel: static split, 768-thread CTAs (flags bit 4 forces the generic one)
-        L->fast = !det && can_big && wpc == FAST_T / 32 && sched->batch <= 0 && !diag_generic;
-        if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen);
+        L->fast = can_fast && wpc == FAST_T / 32;
+        if (L->fast) big = true;  // no per-warp scratch
+        L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
+        L->kernel = pick_kernel(csr, part->kind, can_big && wpc > 8);
+        if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, part->max_slots <= 32 ? 1 : 2);
         L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
@@ -1295,7 +1375,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
         while ((uint64_t)sched->count % m == 0) m += 2;
         a.scramble = m % (uint64_t)sched->count ? m : 1;
     }
-    a.period = sched->hot_period > 0 ? sched->hot_period : 8;
+    a.period = sched->hot_period > 0 ? sched->hot_period : 16;
     // effective delay: in-flight warps + the staleness of the hot snapshot
     // (up to period * ctas updates between a CTA's refreshes)
     double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);

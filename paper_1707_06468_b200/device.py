@@ -268,7 +268,7 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self._keep = s
 
-    def run_async(self, count, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=2.0, hot=None,
+    def run_async(self, count, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=4.0, hot=None,
                   hot_period=0, flags=0, stream=None):
         """`count` lock-free updates (asynchronous.py:131-210), continuing the
         sampler stream where the previous call stopped.  ``contention`` = c of

@@ -79,7 +79,7 @@ def run_path(lambdas, solve, rank=None, world=None):
 
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
-                  mode="async", contention=2.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
+                  mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
     """A ``solve(lam)`` closure over one DeviceProblem (uploaded once)."""
     from .device import DeviceProblem
     from .penalties import GroupL2Penalty, L1Penalty

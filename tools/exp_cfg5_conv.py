@@ -17,8 +17,8 @@ print(json.dumps({"n": n, "p": d.n_features, "H": dp.H, "lam_max": lam_max}), fl
 for frac in (1.0, 0.1, 0.01):
     lam = frac * lam_max
     dp.lam2 = lam
-    for tag, kw in (("fast_c2", dict(contention=2.0)), ("fast_c1", dict(contention=1.0)), ("fast_nohot", dict(contention=2.0, hot=False)),
-                    ("generic_c2", dict(contention=2.0, flags=16, hot=False))):
+    for tag, kw in (("c2", dict(contention=2.0)), ("c4", dict(contention=4.0)), ("c2_delta", dict(contention=2.0, flags=32)),
+                    ("c8", dict(contention=8.0))):
         dp.reset_state(); objs = []
         for ep in range(30):
             dp.run_async(n, gamma, seed=3, **kw)
