@@ -117,6 +117,8 @@ typedef struct ps_sched {
 /* ps_sched_t.flags (async only; diagnostics except where noted) */
 #define PS_FLAG_SCRAMBLE 4        /* permute the slot order within the call */
 #define PS_FLAG_GENERIC 16        /* force the generic kernel (no pipelined fast path) */
+#define PS_FLAG_GROUP_WARP 64     /* group lasso: the warp-cooperative kernel even when staging */
+#define PS_FLAG_GROUP_LANE 128    /* group lasso: the lane-per-block kernel without staging */
 #define PS_FLAG_DELTA_ZERO 32     /* commit prox-zeroed coordinates as the delta -x_hat, the
                                      reference's literal scatter_add (asynchronous.py:105-107);
                                      default: store 0 */

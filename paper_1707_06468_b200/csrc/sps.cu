@@ -67,7 +67,7 @@ struct KArgs {
     int32_t hot_shift;    // hot unit r is stored at unit index r << hot_shift
     int32_t hot_unit;     // coordinates per hot unit (1: columns, G: contiguous blocks)
     uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
-    int32_t diag;         // diagnostics: bit5 hot abar credit direct to L2, bit6 hot x commit direct
+    int32_t diag;         // ps_sched_t.flags (PS_FLAG_*)
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -278,7 +278,8 @@ __device__ __noinline__ void hot_flush_group(const KArgs &a, const HotView &h, i
 #pragma unroll
                 for (int c = 0; c < NCOPY; c++) dab += smem_take(pend + (2 * c + 1) * H + s);
                 double *gp = a.coord + 4 * hot_coord(a, s);
-                if (dz != 0.0) red_add(gp, dz);
+                if (z == 0.0 && !(a.diag & PS_FLAG_DELTA_ZERO)) atomic_exch(gp, 0.0);
+                else if (dz != 0.0) red_add(gp, dz);
                 if (dab != 0.0) red_add(gp + 1, dab);
                 if (refresh) {
                     smem_dyn[2 * s] = z;
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     // async work split (asynchronous.py:125-128 split_iterations): warp gw owns
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     // kernel parameters used in the loop, hoisted
@@ -960,7 +961,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 33) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
         for (int r = threadIdx.x; r < HB; r += blockDim.x) bcnt[r] = 0;
         __syncthreads();
     }
@@ -997,9 +998,13 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
             double part = 0.0;
             for (int t0 = 0; t0 < g; t0 += bpc) {
                 const int t = t0 + tb;
-                const bool on = tb < bpc && t < g;
-                const int src = on ? (int)__fns(leaders, 0, t + 1) : 0;
+                const bool on0 = tb < bpc && t < g;
+                const int src = on0 ? (int)__fns(leaders, 0, t + 1) : 0;
                 const int B = __shfl_sync(FULL, blk, src);
+                if (on0) {
+                    wx[t * G + qd] = wab[t * G + qd] = wd[t * G + qd] = 0.0;
+                }
+                const bool on = on0 && (int64_t)B * G + qd < a.p;  // ragged last block
                 if (on) {
                     const int s2 = t * G + qd;
                     const int64_t c = (int64_t)B * G + qd;
@@ -1046,9 +1051,10 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
             // ---- pass 2: u, block norms, group shrinkage, commit x on T_i
             for (int t0 = 0; t0 < g; t0 += bpc) {
                 const int t = t0 + tb;
-                const bool on = tb < bpc && t < g;
-                const int src = on ? (int)__fns(leaders, 0, t + 1) : 0;
+                const bool on0 = tb < bpc && t < g;
+                const int src = on0 ? (int)__fns(leaders, 0, t + 1) : 0;
                 const int B = __shfl_sync(FULL, blk, src);
+                const bool on = on0 && (int64_t)B * G + qd < a.p;
                 const int s2 = t * G + qd;
                 double xh = 0.0, u = 0.0, d = 0.0;
                 const bool hot = B < hbl && (B & (S - 1)) == 0;
@@ -1161,6 +1167,234 @@ template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int los
     if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, NC, FAST_T>;
     return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, NC, FAST_T>;
 }
+// ---------------------------------------------------------------------------
+// Group lasso, lane per block (contiguous blocks of G in {2,4,5,8,10,16},
+// rows of <= 32 nonzeros; BASELINE config 5).  The leader lane of each of the
+// row's distinct blocks (__match_any_sync on col / G) owns the whole block:
+// it issues the G coordinate loads back to back, computes u on the block,
+// its squared norm in registers, the group shrinkage (penalties.py:103-108)
+// and commits the G coordinates; no shuffles inside a block.  The row
+// values reach their block owner through per-warp shared memory.  Pipelined
+// like sps_fast_kernel (next row prefetched, abar credit deferred one update).
+template <typename VT, typename PT, int LOSS, int G, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
+{
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int nwib = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * nwib + wib;
+    // shared memory: [hot staging area | dirty words] then per-warp row values
+    HotView h = hot_view(smem_dyn, a.H);
+    unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
+    double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
+    const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
+    double *wa = smem_dyn + hdr + (int64_t)wib * (32 * G);  // row value per (leader lane, q)
+    if (a.H > 0) {
+        for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
+            const double *g = a.coord + 4 * hot_coord(a, s);
+            reinterpret_cast<double2 *>(h.xab)[s] = ld_cg2(g);
+            h.d[s] = __ldg(g + 2);
+        }
+        for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
+        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
+        __syncthreads();
+    }
+    double *const coord = a.coord;
+    double *const alpha = a.alpha;
+    const double gamma = a.gamma, lambda1 = a.lambda1, kappa = a.kappa, kappa_hot = a.kappa_hot, lam2 = a.lam2;
+    const bool store_zero = !(a.diag & PS_FLAG_DELTA_ZERO);
+    const uint64_t seed = a.seed, base = a.slot_base, nrows = (uint64_t)a.n;
+    const double inv_n = 1.0 / a.n_d;
+    const int64_t p = a.p;
+    const int shift = a.hot_shift;
+    const int hbl = (a.H / G) << shift;  // hot blocks: multiples of 2^shift below this
+    const int64_t nwarps = (int64_t)gridDim.x * nwib;
+    const int64_t q0 = a.count / nwarps, rr = a.count % nwarps;
+    uint64_t slot = (uint64_t)(gw * q0 + min(gw, rr));
+    const uint64_t slot_end = slot + (uint64_t)(q0 + (gw < rr ? 1 : 0));
+    int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, nwib) : 0;
+
+    int pcol = -1, pslot = -1;
+    double pval = 0.0, pnw = 0.0, prep = 0.0;
+    if (slot < slot_end) {
+        Row<VT, 1> cur;
+        fetch_rowc<VT, PT, 1>(a, sample_row(seed, base + slot, nrows), lane, cur, true);
+        while (true) {
+            const int col = cur.col[0];
+            const bool act = col >= 0;
+            const int blk = act ? col / G : -1 - lane;
+            const unsigned peers = __match_any_sync(FULL, blk);
+            const bool leader = act && (__ffs(peers) - 1) == lane;
+            const int lead = __ffs(peers) - 1;
+            // staged block: its G slots start at sb
+            const int sb = (act && blk < hbl && (blk & ((1 << shift) - 1)) == 0) ? (blk >> shift) * G : -1;
+            // ---- leaders: the block's G records (x^, abar^) and its weight D
+            double xh[G], ab[G], d = 0.0;
+            const int64_t c0 = (int64_t)blk * G;
+            const int nq = leader ? (int)min((int64_t)G, p - c0) : 0;  // ragged last block
+            if (leader) {
+                if (sb >= 0) {
+#pragma unroll
+                    for (int q = 0; q < G; q++) {
+                        double2 v = reinterpret_cast<const double2 *>(h.xab)[sb + q];
+                        xh[q] = v.x;
+                        ab[q] = v.y;
+                    }
+                    d = h.d[sb];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < G; q++) {
+                        double2 v = q < nq ? ld_cg2(coord + 4 * (c0 + q)) : make_double2(0.0, 0.0);
+                        xh[q] = v.x;
+                        ab[q] = v.y;
+                    }
+                    d = __ldg(coord + 4 * c0 + 2);
+                }
+            }
+            double old = 0.0;
+            if (lane == 0) old = ld_cg(alpha + cur.i);
+            // ---- abar credit of the previous update
+            {
+                const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+                if (pcol >= 0) {
+                    if (pslot >= 0) {
+                        atomicAdd(pab + pslot, t * pval);
+                        mark_dirty(dirty, pslot);
+                    } else {
+                        red_add(coord + 4 * (int64_t)pcol + 1, t * pval);
+                    }
+                }
+            }
+            // ---- prefetch the next row
+            const bool more = slot + 1 < slot_end;
+            slot++;
+            Row<VT, 1> nxt;
+            fetch_rowc<VT, PT, 1>(a, more ? sample_row(seed, base + slot, nrows) : cur.i, lane, nxt, more);
+            // ---- row values to their block owner
+            if (leader) {
+#pragma unroll
+                for (int q = 0; q < G; q++) wa[lane * G + q] = 0.0;
+            }
+            __syncwarp();
+            const double cval = widen(cur.val[0]);
+            if (act) wa[lead * G + (col - blk * G)] = cval;
+            __syncwarp();
+            double part = 0.0;
+            if (leader) {
+#pragma unroll
+                for (int q = 0; q < G; q++) part += wa[lane * G + q] * xh[q];
+            }
+            const double margin = warp_sum(part);
+            old = __shfl_sync(FULL, old, 0);
+            const double nw = deriv_t<LOSS>(margin, widen(cur.y));
+            const double ds = nw - old;
+            if (leader) {
+                const double gB = gamma * fmin(1.0, (sb >= 0 ? kappa_hot : kappa) * d);
+                double ss = 0.0;
+#pragma unroll
+                for (int q = 0; q < G; q++) {
+                    double v = d * (ab[q] + lambda1 * xh[q]);
+                    v += ds * wa[lane * G + q];
+                    const double u = xh[q] - gB * v;
+                    ab[q] = u;  // reuse
+                    ss += u * u;
+                }
+                const double f = group_factor(sqrt(ss), gB * d, lam2);
+                if (f == 0.0 && store_zero) {
+                    // the prox zeroed the block: store it
+#pragma unroll
+                    for (int q = 0; q < G; q++) {
+                        if (q < nq) {
+                            if (sb >= 0) {
+                                drop_pending_x(h, sb + q);
+                                h.xab[2 * (sb + q)] = 0.0;  // this CTA sees its own store
+                            }
+                            atomic_exch(coord + 4 * (c0 + q), 0.0);
+                        }
+                    }
+                } else if (sb >= 0) {
+#pragma unroll
+                    for (int q = 0; q < G; q++) {
+                        atomicAdd(px + sb + q, ab[q] * f - xh[q]);
+                        mark_dirty(dirty, sb + q);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < G; q++)
+                        if (q < nq) red_add(coord + 4 * (c0 + q), ab[q] * f - xh[q]);
+                }
+            }
+            double rep = 0.0;
+            if (lane == 0) rep = atomic_exch(alpha + cur.i, nw);
+            pnw = nw;
+            prep = rep;
+            pcol = col;
+            pslot = sb >= 0 ? sb + (col - blk * G) : -1;
+            pval = cval;
+            if (a.H > 0 && --until_flush == 0) {
+                hot_flush(a, h, dirty, lane, true);
+                until_flush = a.period;
+            }
+            __syncwarp();
+            if (!more) break;
+            cur = nxt;
+        }
+        const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+        if (pcol >= 0) {
+            if (pslot >= 0) {
+                atomicAdd(pab + pslot, t * pval);
+                mark_dirty(dirty, pslot);
+            } else {
+                red_add(coord + 4 * (int64_t)pcol + 1, t * pval);
+            }
+        }
+    }
+    if (lane == 0) {
+        int64_t mine = q0 + (gw < rr ? 1 : 0);
+        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
+    }
+    if (a.H > 0) {
+        hot_async_drain();
+        __syncthreads();
+        if (wib == 0) {
+            dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));
+            __syncwarp();
+            hot_flush(a, h, dirty, lane, false);
+        }
+        hot_async_drain();
+    }
+}
+
+// 768 threads (85 registers) while the block's 2G doubles fit, else 512
+static constexpr int glane_threads(int G) { return G <= 5 ? 768 : 512; }
+template <typename VT, typename PT, int G> static void *kernel_ptr_glane(int loss)
+{
+    if (loss == PS_LOSS_LOGISTIC)
+        return (void *)sps_group_lane_kernel<VT, PT, PS_LOSS_LOGISTIC, G, glane_threads(G)>;
+    return (void *)sps_group_lane_kernel<VT, PT, PS_LOSS_SQUARED, G, glane_threads(G)>;
+}
+template <int G> static void *pick_glane_g(const ps_csr_t *csr, int loss)
+{
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) return kernel_ptr_glane<double, long long, G>(loss);
+    if (f64) return kernel_ptr_glane<double, int, G>(loss);
+    if (i64) return kernel_ptr_glane<float, long long, G>(loss);
+    return kernel_ptr_glane<float, int, G>(loss);
+}
+static bool glane_ok(int G) { return G == 2 || G == 4 || G == 5 || G == 8 || G == 10 || G == 16; }
+static void *pick_glane(const ps_csr_t *csr, int loss, int G)
+{
+    switch (G) {
+    case 2: return pick_glane_g<2>(csr, loss);
+    case 4: return pick_glane_g<4>(csr, loss);
+    case 5: return pick_glane_g<5>(csr, loss);
+    case 8: return pick_glane_g<8>(csr, loss);
+    case 10: return pick_glane_g<10>(csr, loss);
+    default: return pick_glane_g<16>(csr, loss);
+    }
+}
+
 constexpr int GROUP_T = 512;
 template <typename VT, typename PT> static void *kernel_ptr_group(int loss)
 {
@@ -1242,17 +1476,32 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         L->H = std::min(HOT_MAX, std::max(0, (int)sched->hot_cols));
     int wpc;
     L->fast = false;
-    if (group_fast) {
+    if (group_fast && glane_ok(part->G) && (sched->hot_cols > 0 || (sched->flags & PS_FLAG_GROUP_LANE)) &&
+        !(sched->flags & PS_FLAG_GROUP_WARP)) {
+        // lane-per-block group kernel; hot blocks staged per CTA like hot columns
+        // (opt-in: staging converges at small lambda but stalls near lambda_max,
+        // see DESIGN.md; the default group path is the warp kernel, unstaged)
+        L->wpc = wpc = (part->G <= 5 ? 768 : 512) / 32;
+        const size_t warp_stage = (size_t)wpc * 32 * part->G * 8;
+        L->H -= L->H % part->G;  // whole blocks
+        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17) * 8 > 220 * 1024) L->H -= part->G;
+        L->kernel = pick_glane(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, part->G);
+        L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
+        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0);
+        L->smem_flag = 0;
+        L->stride = L->M = L->GB = 0;
+        L->gscratch_bytes = 0;
+        L->fast = true;
+    } else if (group_fast) {
         wpc = GROUP_T / 32;
         const size_t warp_stage = (size_t)wpc * 4 * 32 * part->G * 8;
         // keep the CTA within the shared-memory budget: shrink the hot set (whole blocks)
         L->H -= L->H % part->G;  // whole blocks
-        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17 + L->H / part->G) * 8 > 220 * 1024)
-            L->H -= part->G;
+        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17) * 8 > 220 * 1024) L->H -= part->G;
         L->kernel = pick_group(csr, prm ? prm->loss : PS_LOSS_LOGISTIC);
         L->wpc = wpc;
         L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
-        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17 + (L->H / part->G + 1) / 2) * 8 : 0);
+        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0);
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
         L->gscratch_bytes = 0;

@@ -39,9 +39,8 @@ def run(tag, phases, hot_max=256):
                       "ms_to_1e-6": sum(ms[:hit]) if hit else None,
                       "gap": [float(f"{g:.2e}") for g in gaps[4::5]], "final": gaps[-1]}), flush=True)
 
-S = dict(contention=2.0, hot_period=16)
+S = dict(contention=4.0, hot_period=16)
 for H in (256, 1024):
-    for hp in (8, 16, 24):
-        for c in (2.0, 4.0, 6.0, 8.0):
-            run(f"H{H}_hp{hp}_c{c}", [(30, dict(S, hot_period=hp, contention=c))], hot_max=H)
-run("H256_hp16_c4_delta", [(30, dict(S, contention=4.0, flags=32))], hot_max=256)
+    for hp in (16, 32, 64):
+        for fl in (0, 512):
+            run(f"H{H}_hp{hp}_fl{fl}", [(30, dict(S, hot_period=hp, flags=fl))], hot_max=H)
