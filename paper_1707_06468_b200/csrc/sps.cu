@@ -189,10 +189,19 @@ __device__ __forceinline__ int64_t hot_coord(const KArgs &a, int s)
     return (((int64_t)r << a.hot_shift) * a.hot_unit) + q;
 }
 
-__device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigned *dirty, int lane, bool refresh)
+struct FlushArgs {  // what the flush needs, by value (keeps KArgs out of local memory)
+    double *coord;
+    int shift, unit;
+};
+__device__ __forceinline__ int64_t hot_coord(const FlushArgs &f, int s)
 {
-    extern __shared__ double smem_dyn[];  // h.* point into it: use explicit shared addressing
-    const int H = h.H;
+    if (f.unit <= 1) return (int64_t)s << f.shift;
+    int r = s / f.unit, q = s - r * f.unit;
+    return (((int64_t)r << f.shift) * f.unit) + q;
+}
+__device__ __noinline__ void hot_flush(const FlushArgs fa, const int H, unsigned *dirty, int lane, bool refresh)
+{
+    extern __shared__ double smem_dyn[];  // the staging area starts the dynamic shared memory
     double *pend = smem_dyn + 3 * H;
     unsigned m = atomicExch(dirty + lane, 0u);
     while (m) {
@@ -206,7 +215,7 @@ __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigne
             dx += smem_take(pend + (2 * c) * H + s);
             dab += smem_take(pend + (2 * c + 1) * H + s);
         }
-        double *g = a.coord + 4 * hot_coord(a, s);
+        double *g = fa.coord + 4 * hot_coord(fa, s);
         if (dx != 0.0) red_add(g, dx);
         if (dab != 0.0) red_add(g + 1, dab);
     }
@@ -216,18 +225,17 @@ __device__ __noinline__ void hot_flush(const KArgs &a, const HotView &h, unsigne
     unsigned rot = 0;
     if (lane == 0) rot = atomicAdd(dirty + 32, 1u);
     rot = __shfl_sync(FULL, rot, 0) & 3u;
-#pragma unroll 4
-    for (int k = 0; k < HOT_PER_LANE; k++) {
+    const int kmax = (H + 31) >> 5;
+    for (int k = 0; k < kmax; k++) {
         int s = lane + 32 * k;
         if (s < H && (k < HOT_TIER0 / 32 || (k & 3) == (int)rot)) {
             unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dyn + 2 * s);
-            const double *src = a.coord + 4 * hot_coord(a, s);
+            const double *src = fa.coord + 4 * hot_coord(fa, s);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
-
 __device__ __forceinline__ void hot_async_drain() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Group-lasso flush (sps_group_kernel): hot blocks accumulate the samples'
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
             __syncwarp();
         }
         if (a.H > 0 && --until_flush == 0) {
-            hot_flush(a, h, dirty, lane, true);
+            hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
             until_flush = a.period;
         }
     }
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
         if (wib == 0) {
             dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));  // every slot
             __syncwarp();
-            hot_flush(a, h, dirty, lane, false);
+            hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, false);
         }
         hot_async_drain();
     }
@@ -753,6 +761,26 @@ __device__ __forceinline__ void fetch_rowc(const KArgs &a, int64_t i, int lane, 
     r.y = valid ? __ldg(reinterpret_cast<const VT *>(a.y) + i) : VT(0);
 }
 
+// the row's nonzeros given its extent (row_ptr already read a stage earlier)
+template <typename VT, int NC>
+__device__ __forceinline__ void fetch_cols(const int32_t *__restrict__ colp, const VT *__restrict__ valp,
+                                           const VT *__restrict__ yp, int64_t i, int64_t lo, int k, int lane,
+                                           Row<VT, NC> &r)
+{
+    r.i = i;
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        const int e = lane + 32 * c;
+        r.col[c] = -1;
+        r.val[c] = VT(0);
+        if (e < k) {
+            r.col[c] = __ldg(colp + lo + e);
+            r.val[c] = __ldg(valp + lo + e);
+        }
+    }
+    r.y = k >= 0 ? __ldg(yp + i) : VT(0);
+}
+
 template <typename VT, typename PT, int LOSS, int PEN, int NC, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
 {
@@ -798,9 +826,22 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     for (int c = 0; c < NC; c++) pcol[c] = -1;
     double pnw = 0.0, prep = 0.0;
 
+    const int32_t *const colp = a.col;
+    const VT *const valp = reinterpret_cast<const VT *>(a.val);
+    const VT *const yp = reinterpret_cast<const VT *>(a.y);
+    const void *const rowp = a.row_ptr;
     if (slot < slot_end) {
+        // three-stage pipeline: sample + row extent two updates ahead, the
+        // nonzeros one update ahead, the state reads and the update itself now
         Row<VT, NC> cur;
         fetch_rowc<VT, PT, NC>(a, sample_row(seed, base + slot, nrows), lane, cur, true);
+        int64_t i1 = 0, lo1 = 0;
+        int k1 = -1;
+        if (slot + 1 < slot_end) {
+            i1 = sample_row(seed, base + slot + 1, nrows);
+            lo1 = rp<PT>(rowp, i1);
+            k1 = (int)(rp<PT>(rowp, i1 + 1) - lo1);
+        }
         while (true) {
             // ---- state reads (hot: CTA snapshot in shared memory; cold: one
             // 16-B L2 read + D through the read-only path)
@@ -842,11 +883,18 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                     }
                 }
             }
-            // ---- prefetch the next sample's row (independent of the state)
+            // ---- prefetch: the next row's nonzeros, the row extent after it
             const bool more = slot + 1 < slot_end;
             slot++;
             Row<VT, NC> nxt;
-            fetch_rowc<VT, PT, NC>(a, more ? sample_row(seed, base + slot, nrows) : cur.i, lane, nxt, more);
+            fetch_cols<VT, NC>(colp, valp, yp, more ? i1 : cur.i, lo1, more ? k1 : -1, lane, nxt);
+            int64_t i2 = 0, lo2 = 0;
+            int k2 = -1;
+            if (slot + 1 < slot_end) {
+                i2 = sample_row(seed, base + slot + 1, nrows);
+                lo2 = rp<PT>(rowp, i2);
+                k2 = (int)(rp<PT>(rowp, i2 + 1) - lo2);
+            }
             // ---- margin -> derivative -> prox -> commit x
             double part = 0.0;
 #pragma unroll
@@ -887,11 +935,14 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             pnw = nw;
             prep = rep;
             if (a.H > 0 && --until_flush == 0) {
-                hot_flush(a, h, dirty, lane, true);
+                hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
                 until_flush = a.period;
             }
             if (!more) break;
             cur = nxt;
+            i1 = i2;
+            lo1 = lo2;
+            k1 = k2;
         }
         // last credit
         const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
@@ -917,7 +968,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         if (wib == 0) {
             dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));
             __syncwarp();
-            hot_flush(a, h, dirty, lane, false);
+            hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, false);
         }
         hot_async_drain();
     }
@@ -1333,7 +1384,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
             pslot = sb >= 0 ? sb + (col - blk * G) : -1;
             pval = cval;
             if (a.H > 0 && --until_flush == 0) {
-                hot_flush(a, h, dirty, lane, true);
+                hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
                 until_flush = a.period;
             }
             __syncwarp();
@@ -1360,7 +1411,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
         if (wib == 0) {
             dirty[lane] = HOT_PER_LANE >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - HOT_PER_LANE));
             __syncwarp();
-            hot_flush(a, h, dirty, lane, false);
+            hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, false);
         }
         hot_async_drain();
     }
