@@ -235,6 +235,8 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
     (asynchronous.py:213-230) on the RELATIVE gap (F - F*)/|F*|."""
     import math
 
+    dp.reset_state()  # untimed warm-up of the checkpointed path (side stream, objective kernels)
+    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc)
     dp.reset_state()
     its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc)
     rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
@@ -357,7 +359,7 @@ def main():
     f = data.features
     h2d = f.row_offsets.size * 4 + f.col_indices.size * 4 + f.values.size * 4 + data.labels.size * 4
     d2h = data.n_features * 8 + 2 * 3 * 8
-    for s in range(args.e2e_steps):
+    for s in range(-1, args.e2e_steps):  # s = -1: untimed warm-up call
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tr = pb.run_async(data, loss, pen, part,
@@ -365,7 +367,8 @@ def main():
                                          checkpoint_every=total), index=index)
         _ = tr.final_x[0]
         torch.cuda.synchronize()
-        e2e_times.append(time.perf_counter() - t0)
+        if s >= 0:
+            e2e_times.append(time.perf_counter() - t0)
         del tr
     e2e_val = total / float(np.mean(e2e_times))
     if dist:

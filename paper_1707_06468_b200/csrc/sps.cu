@@ -1208,15 +1208,20 @@ template <typename VT, typename PT> static void *kernel_ptr_big()
 {
     return (void *)sps_kernel<VT, PT, PS_PART_SINGLETON, 1024>;
 }
-constexpr int FAST_T = 768;
-template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int loss, int pen)
+// fast kernel CTA sizes: 32 warps (default) or 24 warps (warps_per_cta = 24)
+constexpr int FAST_T = 1024, FAST_T_SMALL = 768;
+template <typename VT, typename PT, int NC, int T> static void *kernel_ptr_fast_t(int loss, int pen)
 {
     if (loss == PS_LOSS_LOGISTIC) {
-        if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, NC, FAST_T>;
-        return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, NC, FAST_T>;
+        if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, NC, T>;
+        return (void *)sps_fast_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, NC, T>;
     }
-    if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, NC, FAST_T>;
-    return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, NC, FAST_T>;
+    if (pen == PS_PEN_L1) return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, NC, T>;
+    return (void *)sps_fast_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, NC, T>;
+}
+template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int loss, int pen, bool small)
+{
+    return small ? kernel_ptr_fast_t<VT, PT, NC, FAST_T_SMALL>(loss, pen) : kernel_ptr_fast_t<VT, PT, NC, FAST_T>(loss, pen);
 }
 // ---------------------------------------------------------------------------
 // Group lasso, lane per block (contiguous blocks of G in {2,4,5,8,10,16},
@@ -1460,19 +1465,19 @@ static void *pick_group(const ps_csr_t *csr, int loss)
     if (i64) return kernel_ptr_group<float, long long>(loss);
     return kernel_ptr_group<float, int>(loss);
 }
-static void *pick_fast(const ps_csr_t *csr, int loss, int pen, int nc)
+static void *pick_fast(const ps_csr_t *csr, int loss, int pen, int nc, bool small)
 {
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
     if (nc == 1) {
-        if (f64 && i64) return kernel_ptr_fast<double, long long, 1>(loss, pen);
-        if (f64) return kernel_ptr_fast<double, int, 1>(loss, pen);
-        if (i64) return kernel_ptr_fast<float, long long, 1>(loss, pen);
-        return kernel_ptr_fast<float, int, 1>(loss, pen);
+        if (f64 && i64) return kernel_ptr_fast<double, long long, 1>(loss, pen, small);
+        if (f64) return kernel_ptr_fast<double, int, 1>(loss, pen, small);
+        if (i64) return kernel_ptr_fast<float, long long, 1>(loss, pen, small);
+        return kernel_ptr_fast<float, int, 1>(loss, pen, small);
     }
-    if (f64 && i64) return kernel_ptr_fast<double, long long, 2>(loss, pen);
-    if (f64) return kernel_ptr_fast<double, int, 2>(loss, pen);
-    if (i64) return kernel_ptr_fast<float, long long, 2>(loss, pen);
-    return kernel_ptr_fast<float, int, 2>(loss, pen);
+    if (f64 && i64) return kernel_ptr_fast<double, long long, 2>(loss, pen, small);
+    if (f64) return kernel_ptr_fast<double, int, 2>(loss, pen, small);
+    if (i64) return kernel_ptr_fast<float, long long, 2>(loss, pen, small);
+    return kernel_ptr_fast<float, int, 2>(loss, pen, small);
 }
 
 static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
@@ -1521,7 +1526,8 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     // CTA per SM (fewest hot-flush agents, full register budget); else 8-warp CTAs
     const bool can_big = part->kind == PS_PART_SINGLETON && part->max_slots <= 32;
     const bool can_fast = part->kind == PS_PART_SINGLETON && part->max_slots <= 64 && !det && sched->batch <= 0 &&
-                          !diag_generic && (sched->warps_per_cta <= 0 || sched->warps_per_cta == FAST_T / 32);
+                          !diag_generic && (sched->warps_per_cta <= 0 || sched->warps_per_cta == FAST_T / 32 ||
+                                            sched->warps_per_cta == FAST_T_SMALL / 32);
     L->H = 0;
     if (!det && (part->kind == PS_PART_SINGLETON || group_fast))
         L->H = std::min(HOT_MAX, std::max(0, (int)sched->hot_cols));
@@ -1559,14 +1565,16 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         L->fast = true;
     } else {
         L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
-        wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : ((can_big || can_fast) ? 24 : 8));
+        wpc = det ? 1 : (sched->warps_per_cta > 0 ? sched->warps_per_cta : (can_fast ? FAST_T / 32 : (can_big ? 24 : 8)));
         bool big = can_big && wpc > 8;
         // the pipelined fast kernel: static split, 768-thread CTAs (flags bit 4 forces the generic one)
-        L->fast = can_fast && wpc == FAST_T / 32;
+        L->fast = can_fast && (wpc == FAST_T / 32 || wpc == FAST_T_SMALL / 32);
         if (L->fast) big = true;  // no per-warp scratch
         L->wpc = wpc = std::min(std::max(wpc, 1), big ? 32 : 8);
         L->kernel = pick_kernel(csr, part->kind, can_big && wpc > 8);
-        if (L->fast) L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, part->max_slots <= 32 ? 1 : 2);
+        if (L->fast)
+            L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, part->max_slots <= 32 ? 1 : 2,
+                                  wpc == FAST_T_SMALL / 32);
         L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
@@ -1675,7 +1683,9 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
         while ((uint64_t)sched->count % m == 0) m += 2;
         a.scramble = m % (uint64_t)sched->count ? m : 1;
     }
-    a.period = sched->hot_period > 0 ? sched->hot_period : 16;
+    // default flush period: 24 updates per warp for the singleton fast kernel
+    // (32 warps per CTA), 16 elsewhere (tools/exp_floor2.py sweeps)
+    a.period = sched->hot_period > 0 ? sched->hot_period : ((L.fast && part->kind == PS_PART_SINGLETON && L.wpc == FAST_T / 32) ? 24 : 16);
     // effective delay: in-flight warps + the staleness of the hot snapshot
     // (up to period * ctas updates between a CTA's refreshes)
     double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);

@@ -28,7 +28,7 @@ def run(tag, phases, hot_max=256):
         for _ in range(epochs):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            dp.run_async(n, gamma, seed=11, ctas=148, warps_per_cta=24, **kw)
+            dp.run_async(n, gamma, seed=11, **kw)
             e.record()
             torch.cuda.synchronize()
             kms += s.elapsed_time(e)
@@ -40,7 +40,6 @@ def run(tag, phases, hot_max=256):
                       "gap": [float(f"{g:.2e}") for g in gaps[4::5]], "final": gaps[-1]}), flush=True)
 
 S = dict(contention=4.0, hot_period=16)
-for H in (256, 1024):
-    for hp in (16, 32, 64):
-        for fl in (0, 512):
-            run(f"H{H}_hp{hp}_fl{fl}", [(30, dict(S, hot_period=hp, flags=fl))], hot_max=H)
+for hp in (16, 24, 32):
+    for c in (3.0, 4.0, 6.0):
+        run(f"w32_hp{hp}_c{c}", [(30, dict(S, hot_period=hp, contention=c))])
