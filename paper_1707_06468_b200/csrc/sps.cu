@@ -831,17 +831,29 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     const VT *const yp = reinterpret_cast<const VT *>(a.y);
     const void *const rowp = a.row_ptr;
     if (slot < slot_end) {
-        // three-stage pipeline: sample + row extent two updates ahead, the
-        // nonzeros one update ahead, the state reads and the update itself now
+        // pipeline: samples and row extents are drawn 32 at a time (lane L holds
+        // slot first + L) one batch ahead and handed out by shuffles; a row's
+        // nonzeros are fetched one update ahead; the state reads and the update
+        // itself run now
+        const uint64_t first = slot;
+        int64_t bi, blo, ni, nlo;
+        int bk, nk;
+        auto load_batch = [&](uint64_t s0, int64_t &bi_, int64_t &blo_, int &bk_) {
+            const uint64_t sl = s0 + (uint64_t)lane;
+            bi_ = 0;
+            blo_ = 0;
+            bk_ = -1;
+            if (sl < slot_end) {
+                bi_ = sample_row(seed, base + sl, nrows);
+                blo_ = rp<PT>(rowp, bi_);
+                bk_ = (int)(rp<PT>(rowp, bi_ + 1) - blo_);
+            }
+        };
+        load_batch(first, bi, blo, bk);
+        load_batch(first + 32, ni, nlo, nk);
         Row<VT, NC> cur;
-        fetch_rowc<VT, PT, NC>(a, sample_row(seed, base + slot, nrows), lane, cur, true);
-        int64_t i1 = 0, lo1 = 0;
-        int k1 = -1;
-        if (slot + 1 < slot_end) {
-            i1 = sample_row(seed, base + slot + 1, nrows);
-            lo1 = rp<PT>(rowp, i1);
-            k1 = (int)(rp<PT>(rowp, i1 + 1) - lo1);
-        }
+        fetch_cols<VT, NC>(colp, valp, yp, __shfl_sync(FULL, bi, 0), __shfl_sync(FULL, blo, 0),
+                           __shfl_sync(FULL, bk, 0), lane, cur);
         while (true) {
             // ---- state reads (hot: CTA snapshot in shared memory; cold: one
             // 16-B L2 read + D through the read-only path)
@@ -883,18 +895,20 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                     }
                 }
             }
-            // ---- prefetch: the next row's nonzeros, the row extent after it
+            // ---- prefetch: the next row's nonzeros (its extent from the batch)
             const bool more = slot + 1 < slot_end;
             slot++;
-            Row<VT, NC> nxt;
-            fetch_cols<VT, NC>(colp, valp, yp, more ? i1 : cur.i, lo1, more ? k1 : -1, lane, nxt);
-            int64_t i2 = 0, lo2 = 0;
-            int k2 = -1;
-            if (slot + 1 < slot_end) {
-                i2 = sample_row(seed, base + slot + 1, nrows);
-                lo2 = rp<PT>(rowp, i2);
-                k2 = (int)(rp<PT>(rowp, i2 + 1) - lo2);
+            const uint32_t t1 = (uint32_t)(slot - first);
+            if ((t1 & 31u) == 0) {
+                bi = ni;
+                blo = nlo;
+                bk = nk;
+                load_batch(first + t1 + 32, ni, nlo, nk);
             }
+            const int src = (int)(t1 & 31u);
+            Row<VT, NC> nxt;
+            fetch_cols<VT, NC>(colp, valp, yp, __shfl_sync(FULL, bi, src), __shfl_sync(FULL, blo, src),
+                               more ? __shfl_sync(FULL, bk, src) : -1, lane, nxt);
             // ---- margin -> derivative -> prox -> commit x
             double part = 0.0;
 #pragma unroll
@@ -940,9 +954,6 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             }
             if (!more) break;
             cur = nxt;
-            i1 = i2;
-            lo1 = lo2;
-            k1 = k2;
         }
         // last credit
         const double t = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
