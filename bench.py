@@ -188,7 +188,7 @@ def lambda_path_bench(rank, world, epochs):
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     res = {"lambdas": len(lams), "mine": len(mine), "ms": ms, "updates": len(mine) * epochs * n,
-           "bytes_per_update_est": 2 * 4 + 4 + 2 * 8 + 20 * (4 + 4) + 156.3 * 3 * 8 + 20 * 8 + 15.6 * 8}
+           "bytes_per_update": dp.bytes_per_update(), "mean_blocks_per_row": dp.mean_blocks_per_row()}
     return res
 
 
@@ -393,7 +393,10 @@ def main():
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
                  "value": upd / (float(t.item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t.item()),
-                 "n_gpus": world, "algorithmic_bytes_per_update_est": lp_local["bytes_per_update_est"]}
+                 "n_gpus": world, "algorithmic_bytes_per_update": lp_local["bytes_per_update"],
+                 "mean_blocks_per_row": lp_local["mean_blocks_per_row"],
+                 "roofline_frac_per_gpu": upd / (float(t.item()) / 1e3) / world * lp_local["bytes_per_update"] / 1e9
+                 / peak}
 
     big = {}
     if world == 1 and not args.no_big:
@@ -413,7 +416,7 @@ def main():
                        "warps_in_flight": c_used * w_used, "ctas": c_used, "warps_per_cta": w_used,
                        "bytes_per_update": bpu, "value_storage": "fp32", "state": "fp64 x/abar/D/alpha"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "frac_vs_spec_8TBs": achieved / 8000.0, "peak_source": peak_src,
                          "traffic_source": "profiles/ncu_traffic_r01.json (dram read+write per launch)",
                          "note": "config-2 working set (18 MB) is L2-resident: DRAM traffic << algorithmic bytes",
                          "kernel": "sps_fast_kernel<float,int,LOGISTIC,L1,768>", "kernel_ms_avg": kavg,

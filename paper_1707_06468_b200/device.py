@@ -395,10 +395,28 @@ class DeviceProblem:
         else:
             _lib.check(_lib.load().ps_coord_set(self.coord.data_ptr(), self.p, 0, t.data_ptr(), _lib.stream_ptr()))
 
+    def mean_blocks_per_row(self):
+        """g-bar: mean number of distinct blocks per row (contiguous partitions;
+        rows keyed by (row, col // G) on the device)."""
+        if getattr(self, "_gbar", None) is None:
+            torch = self.torch
+            G = int(self.part.G) if self.part_kind == "contiguous" else 1
+            rp = self.row_ptr.to(torch.int64)
+            rows = torch.repeat_interleave(torch.arange(self.n, device=self.device), rp[1:] - rp[:-1])
+            keys = rows * (self.p_dev // G + 1) + self.col.to(torch.int64) // G
+            self._gbar = float(torch.unique(keys).numel()) / self.n
+        return self._gbar
+
     def bytes_per_update(self, mean_k=None):
-        """Algorithmic bytes per update (SURVEY.md §8d formula, singleton):
-        2 s_ptr + s_y + 2 s_st + k (s_idx + s_val + 5 s_st)."""
+        """Algorithmic bytes per update (SURVEY.md §8d formulas).
+        singleton: 2 s_ptr + s_y + 2 s_st + k (s_idx + s_val + 5 s_st);
+        blocks of G (g blocks, m = G g coordinates per row):
+        2 s_ptr + k (s_idx + s_val) + s_y + 2 s_st + 3 m s_st + k s_st + g s_st."""
         s_ptr = 4 if self.row_ptr_type == _lib.I32 else 8
         s_val = 4 if self.value_type == _lib.F32 else 8
         k = self.nnz / self.n if mean_k is None else mean_k
+        if self.part_kind == "contiguous":
+            g = self.mean_blocks_per_row()
+            m = int(self.part.G) * g
+            return 2 * s_ptr + k * (4 + s_val) + s_val + 2 * 8 + 3 * m * 8 + k * 8 + g * 8
         return 2 * s_ptr + s_val + 2 * 8 + k * (4 + s_val + 5 * 8)
