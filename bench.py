@@ -159,7 +159,11 @@ def lambda_path_bench(rank, world, epochs):
     """BASELINE config 5: 16-lambda group-lasso path (lambda_max .. 1e-3 lambda_max),
     independent solves sharded over the ranks (lambda_path.assign), matrix
     replicated, device-timed per rank, max over ranks; value = updates of all
-    solves / that time."""
+    solves / that time.  Each rank runs its lambdas concurrently (one state
+    fork + stream per lambda, SMs split between them); the serial schedule
+    (one lambda at a time on all SMs) is timed too, with the largest relative
+    objective difference between the two schedules."""
+    import numpy as np
     import torch
 
     import paper_1707_06468_b200 as pb
@@ -170,26 +174,39 @@ def lambda_path_bench(rank, world, epochs):
     d, part, loss = cfg["data"], cfg["partition"], cfg["loss"]
     lam_max = pb.group_lambda_max(d, part)
     lams = lp.lambda_grid(lam_max, 16, 1e-3)
-    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async")
-    dp = solve.problem
     mine = lp.assign(lams, world)[rank]
     n = d.n_samples
-    dp.lam2 = lams[mine[0]] if mine else lams[0]
-    dp.reset_state()
-    dp.run_async(n, solve.gamma, seed=99)  # warm-up
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for k in mine:
-        dp.lam2 = lams[k]
-        dp.reset_state()
-        dp.run_async(epochs * n, solve.gamma, seed=k)
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e)
-    res = {"lambdas": len(lams), "mine": len(mine), "ms": ms, "updates": len(mine) * epochs * n,
-           "bytes_per_update": dp.bytes_per_update(), "mean_blocks_per_row": dp.mean_blocks_per_row()}
-    return res
+    out = {"lambdas": len(lams), "mine": len(mine), "updates": len(mine) * epochs * n}
+
+    def timed(solve):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        if solve.batch is not None:
+            res = solve.batch([lams[k] for k in mine])
+        else:
+            res = [solve(lams[k]) for k in mine]
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e), np.array([r["objective"] for r in res])
+
+    conc = max(1, len(mine))
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=conc)
+    if solve.batch is not None:
+        solve.batch([lams[k] for k in mine])  # warm-up
+    else:
+        solve(lams[mine[0]] if mine else lams[0])
+    ms_c, obj_c = timed(solve)
+    out.update(ms=ms_c, concurrent=conc, bytes_per_update=solve.problem.bytes_per_update(),
+               mean_blocks_per_row=solve.problem.mean_blocks_per_row())
+    del solve
+    torch.cuda.empty_cache()
+    serial = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=1)
+    ms_s, obj_s = timed(serial)
+    del serial
+    torch.cuda.empty_cache()
+    out.update(ms_serial=ms_s,
+               max_rel_obj_diff=float(np.max(np.abs(obj_c - obj_s) / np.abs(obj_s))) if len(mine) else 0.0)
+    return out
 
 
 def big_config_bench(which, peak):
@@ -236,9 +253,11 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
     import math
 
     dp.reset_state()  # untimed warm-up of the checkpointed path (side stream, objective kernels)
-    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc)
+    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc, graph=True)
     dp.reset_state()
-    its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc)
+    # the 30 epochs + checkpoints as one CUDA graph (captured, then replayed and timed on the device)
+    its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc,
+                                                 graph=True)
     rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
     hit = None
     prev_rel, prev_w, prev_it = 1.0, 0.0, 0
@@ -250,7 +269,8 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
         prev_rel, prev_w, prev_it = r, w, it
     return {"target_rel_gap": target, "seconds": hit[0] if hit else None, "epochs": hit[1] if hit else None,
             "reached": hit is not None, "final_rel_gap": rel[-1], "epochs_run": total / n,
-            "fstar": fstar, "wall_incl_evals_s": walls[-1], "checkpoints": "every epoch, pipelined on a side stream"}
+            "fstar": fstar, "wall_incl_evals_s": walls[-1], "checkpoints": "every epoch, pipelined on a side stream, whole sequence replayed as one CUDA graph; "
+                           "times = device %globaltimer stamps after each checkpoint objective"}
 
 
 def main():
@@ -385,18 +405,21 @@ def main():
         del dp
         torch.cuda.empty_cache()
         lp_local = lambda_path_bench(rank, world, args.path_epochs)
-        t = torch.tensor([lp_local["ms"]], device="cuda")
+        t = torch.tensor([lp_local["ms"], lp_local["ms_serial"], lp_local["max_rel_obj_diff"]], device="cuda")
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         upd = 16 * args.path_epochs * 100_000
         lpath = {"workload": "config 5: group-lasso logistic n=1e5 p=1e7 G=10, 16 lambdas log-spaced "
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
-                 "value": upd / (float(t.item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t.item()),
+                 "value": upd / (float(t[0].item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t[0].item()),
+                 "concurrent_per_rank": lp_local["concurrent"],
+                 "serial_value": upd / (float(t[1].item()) / 1e3),
+                 "max_rel_objective_diff_concurrent_vs_serial": float(t[2].item()),
                  "n_gpus": world, "algorithmic_bytes_per_update": lp_local["bytes_per_update"],
                  "mean_blocks_per_row": lp_local["mean_blocks_per_row"],
-                 "roofline_frac_per_gpu": upd / (float(t.item()) / 1e3) / world * lp_local["bytes_per_update"] / 1e9
-                 / peak}
+                 "roofline_frac_per_gpu": upd / (float(t[0].item()) / 1e3) / world * lp_local["bytes_per_update"]
+                 / 1e9 / peak}
 
     big = {}
     if world == 1 and not args.no_big:

@@ -199,6 +199,10 @@ int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_inout, int3
 int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
                    void *stream);
 
+/* *dst = the device's %globaltimer (ns), stream-ordered (capturable into a
+ * CUDA graph): checkpoint timing of DeviceProblem.run_async_checkpointed. */
+int ps_timestamp(unsigned long long *dst, void *stream);
+
 /* coord record <-> plain vectors: field 0 = x, 1 = abar, 2 = D. */
 int ps_coord_get(const double *coord, int64_t p, int32_t field, double *out, void *stream);
 int ps_coord_set(double *coord, int64_t p, int32_t field, const double *in, void *stream);

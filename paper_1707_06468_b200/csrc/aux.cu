@@ -661,6 +661,24 @@ extern "C" int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n
     return PS_OK;
 }
 
+// device timestamp (%globaltimer, ns) into *dst: stream-ordered and capturable,
+// so checkpoint times can be taken inside a CUDA graph (events recorded during
+// capture cannot be used for elapsed-time queries)
+__global__ void k_timestamp(unsigned long long *dst)
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *dst = t;
+}
+
+extern "C" int ps_timestamp(unsigned long long *dst, void *stream)
+{
+    if (!dst) return ps_fail(PS_EINVAL, "null argument");
+    k_timestamp<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+    CK(cudaGetLastError(), "ps_timestamp launch");
+    return PS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Hot-column layout (singleton partitions): the columns appearing in at least
 // max(min_frac * n, theta) rows, theta chosen so at most hot_max qualify, are

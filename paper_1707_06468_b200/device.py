@@ -285,44 +285,73 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self.slot_base += int(count)
 
-    def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, **kw):
+    def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, graph=False, **kw):
         """`total` async updates in segments of `every`; after each segment x is
         snapshotted on the device and the objective of the snapshot is evaluated
         on a side stream while the next segment runs (the reference's monitor,
         asynchronous.py:187-198, without host round trips).  Returns
-        (iterations, objectives, seconds) with times from device events,
-        measured from the first launch to each checkpoint's objective."""
+        (iterations, objectives, seconds) with times from device timestamps
+        (%globaltimer via ps_timestamp), measured from the first launch to the
+        end of each checkpoint's objective.
+
+        ``graph``: the whole sequence (per segment: counter reset, SPS launch,
+        snapshot, objective on the side stream) is captured once into a CUDA
+        graph and replayed, so a segment costs its device time and not the
+        ~0.1 ms of host work per launch (a config-2 epoch is ~0.1 ms of GPU
+        time).  Capture does not execute anything; the replay is the run.
+        Worth it when the segments are short and many (bench time-to-target);
+        the capture + instantiation costs about what eager enqueueing does."""
         torch = self.torch
-        main = torch.cuda.current_stream(self.device)
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device)
         side = self._side
         nseg = -(-int(total) // int(every))
         snaps = [torch.empty(self.p_dev, dtype=torch.float64, device=self.device) for _ in range(min(ring, nseg))]
         outs = torch.zeros((nseg, 4), dtype=torch.float64, device=self.device)
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev_obj = [torch.cuda.Event(enable_timing=True) for _ in range(nseg)]
+        ev_obj = [torch.cuda.Event() for _ in range(nseg)]
         ev_snap = [torch.cuda.Event() for _ in range(nseg)]
+        stamps = torch.zeros(nseg + 1, dtype=torch.int64, device=self.device)  # %globaltimer, ns
         L = _lib.load()
-        ev0.record(main)
-        done, its = 0, []
-        for k in range(nseg):
-            cnt = min(int(every), int(total) - done)
-            self.run_async(cnt, gamma, seed=seed, stream=main, **kw)
-            done += cnt
-            its.append(done)
-            buf = snaps[k % len(snaps)]
-            if k >= len(snaps):
-                main.wait_event(ev_obj[k - len(snaps)])  # ring slot free again
-            _lib.check(L.ps_coord_get(self.coord.data_ptr(), self.p_dev, 0, buf.data_ptr(), _lib.stream_ptr(main)))
-            ev_snap[k].record(main)
-            side.wait_event(ev_snap[k])
-            _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 1,
-                                      outs[k].data_ptr(), _lib.stream_ptr(side)))
-            ev_obj[k].record(side)
+
+        def stamp(k, stream):
+            _lib.check(L.ps_timestamp(stamps.data_ptr() + 8 * k, _lib.stream_ptr(stream)))
+
+        def enqueue(main):
+            stamp(0, main)
+            done, its = 0, []
+            for k in range(nseg):
+                cnt = min(int(every), int(total) - done)
+                self.run_async(cnt, gamma, seed=seed, stream=main, **kw)
+                done += cnt
+                its.append(done)
+                buf = snaps[k % len(snaps)]
+                if k >= len(snaps):
+                    main.wait_event(ev_obj[k - len(snaps)])  # ring slot free again
+                _lib.check(L.ps_coord_get(self.coord.data_ptr(), self.p_dev, 0, buf.data_ptr(),
+                                          _lib.stream_ptr(main)))
+                ev_snap[k].record(main)
+                side.wait_event(ev_snap[k])
+                _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 1,
+                                          outs[k].data_ptr(), _lib.stream_ptr(side)))
+                stamp(k + 1, side)
+                ev_obj[k].record(side)
+            main.wait_event(ev_obj[-1])  # join the side stream
+            return its
+
+        if graph:
+            base0 = self.slot_base
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize(self.device)
+            with torch.cuda.graph(g):
+                its = enqueue(torch.cuda.current_stream(self.device))
+            self.slot_base = base0 + int(total)
+            g.replay()
+        else:
+            its = enqueue(torch.cuda.current_stream(self.device))
         torch.cuda.synchronize(self.device)
         objs = outs[:, :3].sum(dim=1).cpu().numpy().tolist()
-        secs = [ev0.elapsed_time(e) / 1e3 for e in ev_obj]
+        st = stamps.cpu().numpy()
+        secs = [float(st[k + 1] - st[0]) / 1e9 for k in range(nseg)]
         return its, objs, secs
 
     # ------------------------------------------------------------------
@@ -394,6 +423,27 @@ class DeviceProblem:
                                                      t.data_ptr(), _lib.stream_ptr()))
         else:
             _lib.check(_lib.load().ps_coord_set(self.coord.data_ptr(), self.p, 0, t.data_ptr(), _lib.stream_ptr()))
+
+    def fork(self):
+        """Another solve of the same problem on the same GPU (e.g. a second
+        lambda of a path running concurrently on its own stream): shares the
+        device CSR, partition, layout and column statistics; owns x, abar,
+        alpha, the progress counter and the sampler position.  D is copied."""
+        import copy
+
+        torch = self.torch
+        other = copy.copy(self)
+        with torch.cuda.device(self.device):
+            other.coord = self.coord.clone()
+            other.alpha = torch.zeros_like(self.alpha)
+            other.counter = torch.zeros_like(self.counter)
+            other._out = torch.zeros_like(self._out)
+        for name in ("_scratch", "_side", "_grad", "_keep"):
+            if hasattr(other, name):
+                setattr(other, name, None)
+        other.slot_base = 0
+        other.reset_state()
+        return other
 
     def mean_blocks_per_row(self):
         """g-bar: mean number of distinct blocks per row (contiguous partitions;

@@ -64,11 +64,20 @@ def run_path(lambdas, solve, rank=None, world=None):
         world = dist.get_world_size() if dist else 1
     mine = assign(lambdas, world)[rank]
     local = []
-    for k in mine:
+    if getattr(solve, "batch", None) is not None:  # concurrent solves on this rank
         t0 = time.perf_counter()
-        res = dict(solve(lambdas[k]))
-        res.update(index=k, lam=lambdas[k], rank=rank, seconds=time.perf_counter() - t0)
-        local.append(res)
+        outs = solve.batch([lambdas[k] for k in mine])
+        dt = time.perf_counter() - t0
+        for k, res in zip(mine, outs):
+            res = dict(res)
+            res.update(index=k, lam=lambdas[k], rank=rank, seconds=dt)
+            local.append(res)
+    else:
+        for k in mine:
+            t0 = time.perf_counter()
+            res = dict(solve(lambdas[k]))
+            res.update(index=k, lam=lambdas[k], rank=rank, seconds=time.perf_counter() - t0)
+            local.append(res)
     if dist and world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, local)
@@ -79,8 +88,15 @@ def run_path(lambdas, solve, rank=None, world=None):
 
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
-                  mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0):
-    """A ``solve(lam)`` closure over one DeviceProblem (uploaded once)."""
+                  mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0, concurrent=1):
+    """A ``solve(lam)`` closure over one DeviceProblem (uploaded once).
+
+    ``concurrent`` > 1 (async mode): ``solve.batch(lams)`` runs that many
+    lambdas at a time, each on its own stream with its own state
+    (``DeviceProblem.fork``) and 1/concurrent of the SMs.  For config 5 this
+    pays twice: the hottest blocks' updates are spread over ``concurrent``
+    copies of the state instead of queueing on one set of L2 lines, and each
+    solve has fewer updates in flight (smaller tau, larger steps)."""
     from .device import DeviceProblem
     from .penalties import GroupL2Penalty, L1Penalty
     from .saga import resolve_step_size, worker_rng
@@ -111,6 +127,38 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
 
     solve.problem = dp
     solve.gamma = gamma
+    solve.batch = None
+    if concurrent > 1 and samples is None:
+        torch = dp.torch
+        forks = [dp] + [dp.fork() for _ in range(concurrent - 1)]
+        streams = [torch.cuda.Stream(dp.device) for _ in range(concurrent)]
+        sms = torch.cuda.get_device_properties(dp.device).multi_processor_count
+        ctas_each = ctas if ctas > 0 else max(1, sms // concurrent)
+
+        def batch(lams):
+            out = []
+            for w0 in range(0, len(lams), concurrent):
+                wave = lams[w0:w0 + concurrent]
+                torch.cuda.synchronize(dp.device)
+                for f, st, lam in zip(forks, streams, wave):
+                    f.lam2 = float(lam)
+                    f.reset_state(stream=st)
+                    f.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas_each,
+                                warps_per_cta=warps_per_cta, stream=st)
+                torch.cuda.synchronize(dp.device)
+                for f, lam in zip(forks, wave):
+                    parts = f.objective_parts().cpu().numpy()
+                    xt = f.field(0)
+                    r = {"objective": float(parts.sum()), "nnz": int((xt != 0).sum().item()),
+                         "norm": float(torch.linalg.vector_norm(xt).item()), "updates": epochs * n}
+                    if keep_x:
+                        r["x"] = xt.cpu().numpy()
+                    out.append(r)
+            return out
+
+        solve.batch = batch
+        solve.forks = forks
+        solve.streams = streams
     return solve
 
 
@@ -123,12 +171,13 @@ def lambda_max_for(data, partition, penalty_kind="group", device=None):
 
 
 def regularization_path(data, loss, partition, n_lambdas=16, ratio=1e-3, penalty_kind="group", epochs=30,
-                        step="1/2L", seed=0, mode="async", device=None, keep_x=False):
-    """Config 5 end to end on this rank's GPU (call under torchrun for N GPUs)."""
+                        step="1/2L", seed=0, mode="async", device=None, keep_x=False, concurrent=1):
+    """Config 5 end to end on this rank's GPU (call under torchrun for N GPUs).
+    ``concurrent`` lambdas of this rank's share run at a time (device_solver)."""
     lam_max = lambda_max_for(data, partition, penalty_kind, device=device)
     lams = lambda_grid(lam_max, n_lambdas, ratio)
     solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
-                          keep_x=keep_x)
+                          keep_x=keep_x, concurrent=concurrent)
     t0 = time.perf_counter()
     res = run_path(lams, solve)
     return {"lambda_max": lam_max, "lambdas": lams, "results": res, "seconds": time.perf_counter() - t0,

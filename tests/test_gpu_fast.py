@@ -102,3 +102,22 @@ def test_group_lane_kernel_staged_small_lambda(cuda):
     dp.run_async(60 * dp.n, gamma, seed=13, hot=True)
     f = dp.objective()
     assert abs(f - fref) <= ASYNC_TOL * abs(fref), (f, fref)
+
+
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "cuda_graph"])
+def test_checkpointed_run_eager_and_graph(cuda, graph):
+    """run_async_checkpointed: per-epoch device checkpoints (eager launches or
+    one captured CUDA graph) give increasing device timestamps and reach the
+    optimum like a plain run."""
+    data = _instance(20)
+    lam = 1.0 / data.n_samples
+    dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
+                       drop_dead_blocks=True)
+    gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
+    fref = _fstar(dp, gamma)
+    its, objs, secs = dp.run_async_checkpointed(60 * dp.n, dp.n, gamma, seed=3, graph=graph)
+    assert its == [dp.n * (k + 1) for k in range(60)]
+    assert all(b > a for a, b in zip(secs, secs[1:])) and secs[0] > 0
+    assert abs(objs[-1] - fref) <= ASYNC_TOL * abs(fref), (objs[-1], fref)
+    assert objs[-1] == pytest.approx(dp.objective(), rel=1e-14)
+    assert dp.slot_base == 60 * dp.n

@@ -82,3 +82,23 @@ def test_path_sharded_over_two_gloo_ranks_matches_single_process():
     # the path is monotone in sparsity: larger lambda -> fewer nonzeros
     nnz = [g[3] for g in got]
     assert nnz[0] <= nnz[-1]
+
+
+def test_run_path_uses_batch_solver_when_present():
+    """A solver exposing ``batch`` (concurrent solves per rank) gets this
+    rank's lambdas in one call, in assignment order."""
+    calls = []
+
+    def solve(lam):  # pragma: no cover - must not be called
+        raise AssertionError("per-lambda path used")
+
+    def batch(lams):
+        calls.append(list(lams))
+        return [{"objective": lam * 2.0} for lam in lams]
+
+    solve.batch = batch
+    lams = lp.lambda_grid(1.0, 6, 1e-2)
+    res = lp.run_path(lams, solve, rank=0, world=1)
+    assert len(calls) == 1 and calls[0] == [lams[k] for k in lp.assign(lams, 1)[0]]
+    assert [r["index"] for r in res] == list(range(6))
+    assert all(r["objective"] == r["lam"] * 2.0 for r in res)

@@ -14,10 +14,10 @@ solve = lp.device_solver(d, loss, part, epochs=1, mode="async")
 dp, gamma, n = solve.problem, solve.gamma, d.n_samples
 print(json.dumps({"H": dp.H, "hot_shift": dp.hot_shift, "p_dev": dp.p_dev}), flush=True)
 epochs = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-grid = [("hot_f99", dict(hot=True, flags=99 << 16)), ("hot_f99_ad", dict(hot=True, flags=(99 << 16) | 2048)),
-        ("hot_f50_ad", dict(hot=True, flags=2048)), ("hot_wc_ad", dict(hot=True, flags=256 | 2048)),
+grid = [("hot", dict(hot=True)), ("hot_div2", dict(hot=True, flags=2 << 8)), ("hot_div4", dict(hot=True, flags=4 << 8)),
+        ("hot_div16", dict(hot=True, flags=16 << 8)), ("hot_div4_c8", dict(hot=True, flags=4 << 8, contention=8.0)),
         ("warp_cold", dict(hot=False, flags=64))]
-for frac in (1.0, 0.3):
+for frac in (1.0, 0.3, 0.01):
     dp.lam2 = frac * lam_max
     for tag, kw in grid:
         dp.reset_state(); objs = []; ms = 0.0
