@@ -82,21 +82,27 @@ class DeviceProblem:
                 self.row_ptr_type = _lib.I32 if self.row_ptr.dtype == torch.int32 else _lib.I64
                 self.value_type = _lib.F32 if self.val.dtype == torch.float32 else _lib.F64
             else:
-                # ---- CSR upload
-                ro = np.asarray(f.row_offsets)
+                # ---- CSR upload: host arrays go up in their own dtype (a DMA
+                # straight from the caller's buffer, async when it is pinned) and
+                # are narrowed on the device (int64 -> int32 indices, exact
+                # fp64 -> fp32 values), not by a host conversion pass
+                def up(a):
+                    return torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)
+
                 self.row_ptr_type = _lib.I32 if self.nnz < 2 ** 31 - 1 else _lib.I64
-                self.row_ptr = torch.from_numpy(np.ascontiguousarray(
-                    ro, dtype=np.int32 if self.row_ptr_type == _lib.I32 else np.int64)).to(dev)
-                self.col = torch.from_numpy(np.ascontiguousarray(f.col_indices, dtype=np.int32)).to(dev)
-                vals = np.asarray(f.values)
+                ro_d = up(f.row_offsets)
+                self.row_ptr = ro_d.to(torch.int32 if self.row_ptr_type == _lib.I32 else torch.int64)
+                self.col = up(f.col_indices).to(torch.int32)
+                val_d, y_d = up(f.values), up(np.asarray(labels))
                 if value_dtype == "auto":
-                    use32 = _f32_exact(vals) and _f32_exact(labels)
+                    use32 = all(t.dtype == torch.float32 or bool(torch.equal(t.to(torch.float32).to(t.dtype), t))
+                                for t in (val_d, y_d))
                 else:
                     use32 = np.dtype(value_dtype) == np.float32
                 self.value_type = _lib.F32 if use32 else _lib.F64
-                vdt = np.float32 if use32 else np.float64
-                self.val = torch.from_numpy(np.ascontiguousarray(vals, dtype=vdt)).to(dev)
-                self.y = torch.from_numpy(np.ascontiguousarray(labels, dtype=vdt)).to(dev)
+                tdt = torch.float32 if use32 else torch.float64
+                self.val = val_d.to(tdt)
+                self.y = y_d.to(tdt)
             self.csr = _lib.Csr(self.n, self.p, self.nnz, self.row_ptr.data_ptr(), self.col.data_ptr(),
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
             # ---- partition (+ hot-column renumbering for singleton layouts)
