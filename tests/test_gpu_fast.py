@@ -121,3 +121,29 @@ def test_checkpointed_run_eager_and_graph(cuda, graph):
     assert abs(objs[-1] - fref) <= ASYNC_TOL * abs(fref), (objs[-1], fref)
     assert objs[-1] == pytest.approx(dp.objective(), rel=1e-14)
     assert dp.slot_base == 60 * dp.n
+
+
+def test_fast_kernel_empty_and_ragged_rows(cuda):
+    """Rows of 0..48 nonzeros (empty rows included) on the fast kernel: empty
+    rows only move alpha_i toward the loss derivative at margin 0 and the
+    solve still reaches the deterministic optimum."""
+    rng = np.random.default_rng(21)
+    n, p = 8000, 50000
+    ks = rng.integers(0, 49, size=n)
+    ks[::97] = 0
+    cols = [np.sort(rng.choice(2000 if j % 3 else p, size=k, replace=False)) for j, k in enumerate(ks)]
+    ro = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
+    ci = np.concatenate(cols).astype(np.int64)
+    vals = np.concatenate([np.full(k, 1.0 / np.sqrt(max(k, 1)), dtype=np.float32) for k in ks])
+    feats = pb.CsrMatrix(n, p, ro, ci, vals)
+    y = np.where(rng.standard_normal(n) >= 0, 1.0, -1.0)
+    data = pb.Dataset(feats, y)
+    lam = 1.0 / n
+    dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(p),
+                       drop_dead_blocks=True)
+    assert dp.launch_config(dp._sched(dp.n))[1] == 32
+    gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
+    fref = _fstar(dp, gamma)
+    dp.run_async(80 * dp.n, gamma, seed=17)
+    f = dp.objective()
+    assert abs(f - fref) <= ASYNC_TOL * abs(fref), (f, fref)
