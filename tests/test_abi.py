@@ -62,3 +62,16 @@ def test_product_package_never_imports_oracle():
     for f in root.rglob("*.py"):
         src = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), f
+
+
+def test_flag_constants_match_header():
+    """_lib.FLAG_* mirror the PS_FLAG_* defines of include/proxsaga.h."""
+    import re
+    from pathlib import Path
+
+    from paper_1707_06468_b200 import _lib
+
+    text = (Path(__file__).resolve().parents[1] / "include" / "proxsaga.h").read_text()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define PS_FLAG_(\w+)\s+(\d+)", text)}
+    assert defs == {"SCRAMBLE": _lib.FLAG_SCRAMBLE, "GENERIC": _lib.FLAG_GENERIC, "DELTA_ZERO": _lib.FLAG_DELTA_ZERO,
+                    "GROUP_WARP": _lib.FLAG_GROUP_WARP, "GROUP_LANE": _lib.FLAG_GROUP_LANE}

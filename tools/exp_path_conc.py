@@ -12,8 +12,9 @@ d, part, loss = cfg["data"], cfg["partition"], cfg["loss"]
 lams = lp.lambda_grid(pb.group_lambda_max(d, part), 16, 1e-3)
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 ref = None
+flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8,16").split(",")]:
-    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=K)
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=K, flags=flags)
     if K > 1:
         solve.batch(lams[:K])  # warm
     else:
