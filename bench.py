@@ -195,16 +195,19 @@ def lambda_path_bench(rank, world, epochs):
         solve.batch([lams[k] for k in mine])  # warm-up
     else:
         solve(lams[mine[0]] if mine else lams[0])
-    ms_c, obj_c = timed(solve)
-    out.update(ms=ms_c, concurrent=conc, bytes_per_update=solve.problem.bytes_per_update(),
-               mean_blocks_per_row=solve.problem.mean_blocks_per_row())
+    reps_c = [timed(solve) for _ in range(3)]
+    ms_c, obj_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
+    out.update(ms=ms_c, ms_reps=[r[0] for r in reps_c], concurrent=conc,
+               bytes_per_update=solve.problem.bytes_per_update(), mean_blocks_per_row=solve.problem.mean_blocks_per_row())
     del solve
     torch.cuda.empty_cache()
     serial = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=1)
-    ms_s, obj_s = timed(serial)
+    serial(lams[mine[0]] if mine else lams[0])  # warm-up
+    reps_s = [timed(serial) for _ in range(3)]
+    ms_s, obj_s = sorted(reps_s, key=lambda r: r[0])[1]
     del serial
     torch.cuda.empty_cache()
-    out.update(ms_serial=ms_s,
+    out.update(ms_serial=ms_s, ms_serial_reps=[r[0] for r in reps_s],
                max_rel_obj_diff=float(np.max(np.abs(obj_c - obj_s) / np.abs(obj_s))) if len(mine) else 0.0)
     return out
 
@@ -425,7 +428,8 @@ def main():
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
                  "value": upd / (float(t[0].item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t[0].item()),
-                 "concurrent_per_rank": lp_local["concurrent"],
+                 "concurrent_per_rank": lp_local["concurrent"], "rank0_ms_reps": lp_local["ms_reps"],
+                 "rank0_serial_ms_reps": lp_local["ms_serial_reps"],
                  "serial_value": upd / (float(t[1].item()) / 1e3),
                  "max_rel_objective_diff_concurrent_vs_serial": float(t[2].item()),
                  "n_gpus": world, "algorithmic_bytes_per_update": lp_local["bytes_per_update"],

@@ -50,7 +50,7 @@ class DeviceProblem:
     """
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
-                 value_dtype="auto", hot_max=256, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
+                 value_dtype="auto", hot_max=512, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
                  _labels=None, _device_csr=None, _shape=None):
         torch = _torch()
         _lib.require_device()
@@ -110,8 +110,8 @@ class DeviceProblem:
             self.H, self.hot_shift, self.perm, self.perm_np, self.p_dev = 0, 0, None, None, self.p
             self.hot_unit = 1 if self.part_kind == "singleton" else int(self.part.G)
             if self.part_kind in ("singleton", "contiguous") and hot_max > 0 and self.n >= hot_min_rows:
-                # hot_max counts staged coordinates: 256 columns, or ~1024 coordinates of whole blocks
-                units = hot_max if self.hot_unit == 1 else max(1, (4 * hot_max) // self.hot_unit)
+                # hot_max columns (singleton), or whole blocks up to 1024 staged coordinates
+                units = hot_max if self.hot_unit == 1 else max(1, min(4 * hot_max, 1024) // self.hot_unit)
                 self._hot_layout(int(units), float(hot_min_frac), int(hot_stride))
             # ---- state
             self.coord = torch.zeros((self.p_dev, 4), dtype=torch.float64, device=dev)

@@ -9,7 +9,10 @@ import paper_1707_06468_b200 as pb
 from paper_1707_06468_b200 import problems
 from bench import time_to_target
 cfg = problems.config2(seed=0)
-dp = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True)
+import os
+dp = pb.DeviceProblem(cfg["data"], cfg["loss"], cfg["penalty"], cfg["partition"], drop_dead_blocks=True,
+                      hot_max=int(os.environ.get("HOT_MAX", "256")))
+print(json.dumps({"H": dp.H}), flush=True)
 n = dp.n
 gamma = pb.resolve_step_size("1/2L", dp.L, n, cfg["loss"].lambda1)
 fstar = json.loads((ROOT / "tests/golden/cfg2_fstar.json").read_text())["fstar"]
@@ -21,7 +24,7 @@ for g in grid.split(","):
     tt = []
     for r in range(3):
         dp.reset_state()
-        its, objs, walls = dp.run_async_checkpointed(30 * n, n, gamma, seed=7 + r, **kw)
+        its, objs, walls = dp.run_async_checkpointed(30 * n, n, gamma, seed=7 + r, graph=True, **kw)
         rel = [(o - fstar) / abs(fstar) for o in objs]
         hit = next((i for i, x in enumerate(rel) if x <= 1e-6), None)
         tt.append((walls[hit] if hit is not None else None, hit + 1 if hit is not None else None))
