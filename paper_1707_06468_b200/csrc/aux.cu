@@ -52,6 +52,26 @@ extern "C" int ps_device_count(void)
         if (_e != cudaSuccess) return ps_cuda_fail(_e, where);             \
     } while (0)
 
+// Scratch of the aux entry points comes from the device's default stream-
+// ordered pool.  Its release threshold defaults to 0, i.e. every synchronize
+// hands freed pages back and the next cudaMallocAsync maps them again (about a
+// millisecond, measured on ps_objective); keep them instead.
+static cudaError_t pool_alloc(void **ptr, size_t bytes, cudaStream_t st)
+{
+    static bool kept[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !kept[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        kept[dev] = true;
+    }
+    return cudaMallocAsync(ptr, bytes, st);
+}
+
 static int sm_count()
 {
     int dev = 0, sms = 148;
@@ -234,7 +254,7 @@ extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, p
 
     // tmp: [max_sq u64][maxc u64][dead u64][max_nnz i32][max_slots i32]
     void *tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, 64, st), "ps_prepare alloc");
+    CK(pool_alloc(&tmp, 64, st), "ps_prepare alloc");
     CK(cudaMemsetAsync(tmp, 0, 64, st), "ps_prepare memset");
     unsigned long long *max_sq = (unsigned long long *)tmp;
     unsigned long long *maxc = max_sq + 1, *dead = max_sq + 2;
@@ -382,7 +402,7 @@ extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps
     cudaStream_t st = (cudaStream_t)stream;
     const int G1 = std::max(1, sm_count() * 4);  // CTAs per partial pass (fixed -> deterministic)
     double *parts = nullptr;
-    CK(cudaMallocAsync((void **)&parts, sizeof(double) * (3 * G1 + 3), st), "ps_objective alloc");
+    CK(pool_alloc((void **)&parts, sizeof(double) * (3 * G1 + 3), st), "ps_objective alloc");
     double *sums = parts + 3 * G1;
     int64_t n = csr->n_rows, p = csr->n_cols;
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
@@ -548,7 +568,7 @@ extern "C" int ps_fixed_point_residual(const ps_csr_t *csr, const ps_part_t *par
     if (r) return r;
     const int G1 = std::max(1, sm_count() * 4);
     double *parts = nullptr;
-    CK(cudaMallocAsync((void **)&parts, sizeof(double) * G1, st), "ps_fixed_point_residual alloc");
+    CK(pool_alloc((void **)&parts, sizeof(double) * G1, st), "ps_fixed_point_residual alloc");
     if (prm->penalty == PS_PEN_GROUP) {
         int64_t nb = part->kind == PS_PART_SINGLETON ? csr->n_cols : part->n_blocks;
         k_fp_group<<<G1, 256, 0, st>>>(coord, grad, csr->n_cols, part->kind, part->G, nb, part->blk_ptr,
@@ -899,8 +919,8 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
     unsigned long long *cnt = nullptr;
     int32_t *cand = nullptr;
     const int64_t cap = std::min<int64_t>(nu, 1 << 24);
-    CK(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long), st), "ps_hot_layout alloc");
-    CK(cudaMallocAsync((void **)&cand, sizeof(int32_t) * std::max<int64_t>(cap, 1), st), "ps_hot_layout alloc");
+    CK(pool_alloc((void **)&cnt, sizeof(unsigned long long), st), "ps_hot_layout alloc");
+    CK(pool_alloc((void **)&cand, sizeof(int32_t) * std::max<int64_t>(cap, 1), st), "ps_hot_layout alloc");
     CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "ps_hot_layout memset");
     k_collect_ge<<<grid, 256, 0, st>>>(counts_ws, nu, lo, cand, cnt, cap);
     unsigned long long m = 0;
@@ -925,8 +945,8 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
     int nb = (int)((nu + chunk - 1) / chunk);
     int64_t *sums = nullptr;
     int32_t *perm_u = nullptr, *inv_u = nullptr;
-    CK(cudaMallocAsync((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
-    CK(cudaMallocAsync((void **)&perm_u, sizeof(int32_t) * std::max<int64_t>(nu, 1) * 2, st), "ps_hot_layout alloc");
+    CK(pool_alloc((void **)&sums, sizeof(int64_t) * std::max(nb, 1), st), "ps_hot_layout alloc");
+    CK(pool_alloc((void **)&perm_u, sizeof(int32_t) * std::max<int64_t>(nu, 1) * 2, st), "ps_hot_layout alloc");
     inv_u = perm_u + nu;
     k_flag_sums<<<nb, 256, 0, st>>>(counts_ws, nu, theta, chunk, sums);
     k_scan_small<<<1, 1024, 0, st>>>(sums, nb);
@@ -1019,7 +1039,7 @@ static int check_indices(const int64_t *idx, int64_t m, int64_t len, cudaStream_
 {
     if (m <= 0) return PS_OK;
     int *bad = nullptr, hbad = 0;
-    CK(cudaMallocAsync((void **)&bad, sizeof(int), st), "check alloc");
+    CK(pool_alloc((void **)&bad, sizeof(int), st), "check alloc");
     CK(cudaMemsetAsync(bad, 0, sizeof(int), st), "check memset");
     k_check_idx<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(idx, m, len, bad);
     CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "check readback");
