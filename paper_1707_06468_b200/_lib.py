@@ -8,9 +8,13 @@ library or a CUDA device is missing, every solver entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libproxsaga.so"
+# A/B experiments: PROXSAGA_LIB points at another build of the same ABI
+if os.environ.get("PROXSAGA_LIB"):
+    LIB_PATH = Path(os.environ["PROXSAGA_LIB"])
 
 PS_OK, PS_EINVAL, PS_ERANGE, PS_ECUDA, PS_ENOMEM = 0, 1, 2, 3, 4
 LOSS = {"logistic": 0, "squared": 1}
