@@ -256,11 +256,15 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
     import math
 
     dp.reset_state()  # untimed warm-up of the checkpointed path (side stream, objective kernels)
-    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc, graph=True)
+    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc, graph=True, gap=True)
     dp.reset_state()
     # the 30 epochs + checkpoints as one CUDA graph (captured, then replayed and timed on the device)
     its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc,
                                                  graph=True)
+    # the same solve with the Fenchel dual (duality gap) also evaluated at every checkpoint
+    dp.reset_state()
+    _, gobjs, gwalls, duals = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc,
+                                                        graph=True, gap=True)
     rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
     hit = None
     prev_rel, prev_w, prev_it = 1.0, 0.0, 0
@@ -272,7 +276,10 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
         prev_rel, prev_w, prev_it = r, w, it
     return {"target_rel_gap": target, "seconds": hit[0] if hit else None, "epochs": hit[1] if hit else None,
             "reached": hit is not None, "final_rel_gap": rel[-1], "epochs_run": total / n,
-            "fstar": fstar, "wall_incl_evals_s": walls[-1], "checkpoints": "every epoch, pipelined on a side stream, whole sequence replayed as one CUDA graph; "
+            "fstar": fstar, "wall_incl_evals_s": walls[-1],
+            "duality_gap": {"final": gobjs[-1] - duals[-1],
+                            "rel_per_epoch": [float(f"{(o - d) / abs(o):.3e}") for o, d in zip(gobjs, duals)],
+                            "seconds_with_gap_checkpoints": gwalls[-1]}, "checkpoints": "every epoch, pipelined on a side stream, whole sequence replayed as one CUDA graph; "
                            "times = device %globaltimer stamps after each checkpoint objective"}
 
 

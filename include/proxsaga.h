@@ -199,6 +199,13 @@ int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_inout, int3
 int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
                    void *stream);
 
+/* Fenchel dual objective at the dual point induced by x (theta_i = -l'(a_i.x, b_i)):
+ * out[0] = D, out[1] = the scaling applied to theta (lambda1 = 0 with L1 / group,
+ * else 1); duality gap = ps_objective - D >= 0.  No reference counterpart (the
+ * north star's "duality-gap evaluation"); formulas in aux.cu. */
+int ps_dual_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
+                      int32_t x_stride, double *out, void *stream);
+
 /* *dst = the device's %globaltimer (ns), stream-ordered (capturable into a
  * CUDA graph): checkpoint timing of DeviceProblem.run_async_checkpointed. */
 int ps_timestamp(unsigned long long *dst, void *stream);

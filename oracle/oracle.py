@@ -164,6 +164,59 @@ class OracleProblem:
         lib().oracle_smooth_gradient(ctypes.byref(self._s), _p(x, _f64p), _p(g, _f64p))
         return g
 
+    def dual_objective(self, x):
+        """Fenchel dual value at theta_i = -l'(a_i.x) (numpy restatement of the
+        formulas ps_dual_objective evaluates; the reference has no dual, so
+        this is pinned only by weak duality and by its zero gap at the optimum)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rows = np.repeat(np.arange(self.n), np.diff(self.row_ptr))
+        z = np.bincount(rows, weights=self.val * x[self.col], minlength=self.n)
+        b = self.y
+        if self.loss == "logistic":
+            t = -b * z
+            with np.errstate(over="ignore"):
+                sig = np.where(t > 0, 1.0 / (1.0 + np.exp(-t)), np.exp(t) / (1.0 + np.exp(t)))
+            s = -b * sig
+        else:
+            s = z - b
+
+        def conj(sv):
+            if self.loss == "logistic":
+                t = -b * sv
+                r = np.zeros_like(t)
+                pos, lt1 = t > 0, t < 1
+                r[pos] += t[pos] * np.log(t[pos])
+                r[lt1] += (1 - t[lt1]) * np.log1p(-t[lt1])
+                return r
+            return 0.5 * sv * sv + sv * b
+
+        w = np.bincount(self.col, weights=self.val * s[rows], minlength=self.p)
+        v = -w / self.n
+        l1, lam2 = self.lambda1, self.lam2
+        if self.penalty == "group":
+            norms = np.array([np.linalg.norm(v[self.blk_coords[self.blk_ptr[k]:self.blk_ptr[k + 1]]])
+                              for k in range(self.n_blocks)])
+            vmax = norms.max() if len(norms) else 0.0
+            gstar = np.sum(np.maximum(norms - lam2, 0.0) ** 2) / (2 * l1) if l1 > 0 else 0.0
+        else:
+            vmax = np.abs(v).max() if len(v) else 0.0
+            if self.penalty == "l1":
+                gstar = np.sum(np.maximum(np.abs(v) - lam2, 0.0) ** 2) / (2 * l1) if l1 > 0 else 0.0
+            elif self.penalty == "box":
+                if l1 > 0:
+                    c = np.clip(v / l1, self.lo, self.hi)
+                    gstar = np.sum(v * c - 0.5 * l1 * c * c)
+                else:
+                    gstar = np.sum(np.maximum(v * self.lo, v * self.hi))
+            else:
+                if l1 > 0:
+                    gstar = np.sum(v * v) / (2 * l1)
+                else:
+                    return -np.inf if vmax > 0 else -np.sum(conj(s)) / self.n
+        if l1 <= 0 and self.penalty in ("l1", "group") and vmax > lam2:
+            s = s * (lam2 / vmax)
+        return float(-np.sum(conj(s)) / self.n - gstar)
+
     def fixed_point_residual(self, x, gamma):
         x = np.ascontiguousarray(x, dtype=np.float64)
         return float(lib().oracle_fixed_point_residual(ctypes.byref(self._s), _p(x, _f64p), float(gamma)))

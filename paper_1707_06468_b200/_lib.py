@@ -33,6 +33,7 @@ EXPORTS = (
     "ps_coord_get_perm", "ps_coord_set_perm", "ps_atomic_gather",
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels", "ps_timestamp",
+    "ps_dual_objective",
 )
 
 _vp = ctypes.c_void_p
@@ -101,6 +102,7 @@ def load():
         "ps_prox": (_i32, [_P(Params), _vp, _vp, _i64, _vp, _vp]),
         "ps_state_reset": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
         "ps_timestamp": (_i32, [_vp, _vp]),
+        "ps_dual_objective": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _i32, _vp, _vp]),
         "ps_hot_layout": (_i32, [_P(Csr), _vp, _vp, _i32, _i32, _f64, _P(_i32), _vp, _vp, _P(_i32), _P(_i64),
                                  _vp]),
         "ps_coord_get_perm": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),

@@ -556,6 +556,223 @@ __global__ void __launch_bounds__(256) k_fp_group(const double *coord, const dou
     block_sum_store(acc, parts);
 }
 
+// ---------------------------------------------------------------------------
+// Fenchel dual objective (duality gap = primal - dual, SURVEY §8 "on-device
+// objective and duality-gap evaluation").  No reference counterpart (parity
+// unpinned; the oracle restates the same formulas in numpy).
+//   P(x) = (1/n) sum_i l(a_i.x, b_i) + (lambda1/2)||x||^2 + h(x)
+//   D(theta) = -(1/n) sum_i l*(-theta_i) - g*((1/n) A^T theta),  g = lambda1/2||.||^2 + h
+// at the dual point induced by x: theta_i = -l'(a_i.x, b_i) (= -s_i), so
+// v = (1/n) A^T theta = -(1/n) A^T s.  Conjugates:
+//   logistic l*(s) = t log t + (1 - t) log(1 - t), t = -b s in [0, 1]; squared l*(s) = s^2/2 + s b;
+//   lambda1 > 0: L1 sum (|v_j| - lam2)_+^2 / (2 lambda1); group sum_B (||v_B|| - lam2)_+^2 / (2 lambda1);
+//                box sum v c - lambda1 c^2 / 2, c = clip(v / lambda1, lo, hi); zero sum v^2 / (2 lambda1);
+//   lambda1 = 0: L1 / group: theta scaled by c = min(1, lam2 / max |v_j| (max ||v_B||)), g* = 0;
+//                box: sum max(v lo, v hi); zero: 0 if v = 0 else +inf.
+__device__ __forceinline__ double loss_conj(int loss, double s, double b)
+{
+    if (loss == PS_LOSS_LOGISTIC) {
+        const double t = -b * s;
+        double r = 0.0;
+        if (t > 0.0) r += t * log(t);
+        if (t < 1.0) r += (1.0 - t) * log1p(-t);
+        return r;
+    }
+    return 0.5 * s * s + s * b;
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double *p, double v)
+{
+    atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+// s_i = l'(a_i.x, b_i) into s[], sum of l*(s_i) per CTA (thread per row)
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(256) k_dual_rows(const void *row_ptr, const int32_t *col, const void *val,
+                                                   const void *y, int64_t n, int loss, const double *x, int xs,
+                                                   double *s_out, double *parts)
+{
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        double z = 0.0;
+        for (int64_t e = lo; e < hi; e++) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+        const double b = rvx<VT>(y, i);
+        const double si = loss_deriv(loss, z, b);
+        s_out[i] = si;
+        acc += loss_conj(loss, si, b);
+    }
+    block_sum_store(acc, parts);
+}
+
+// w = A^T s (warp per row).  Columns below `head` (the Zipf head, where the
+// hot layout also puts the staged columns) are summed in a per-CTA shared
+// array first and flushed once per CTA: a plain global atomic scatter would
+// queue ~n atomics on column 0's sector.
+constexpr int DUAL_HEAD = 12288;  // 96 KB of shared memory
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(512) k_dual_scatter(const void *row_ptr, const int32_t *col, const void *val,
+                                                      int64_t n, int head, const double *s, double *w)
+{
+    extern __shared__ double acc_head[];
+    for (int j = threadIdx.x; j < head; j += blockDim.x) acc_head[j] = 0.0;
+    __syncthreads();
+    int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        const double si = s[i];
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            const int c = col[e];
+            const double v = rvx<VT>(val, e) * si;
+            if (c < head) atomicAdd(acc_head + c, v);
+            else atomicAdd(w + c, v);
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < head; j += blockDim.x)
+        if (acc_head[j] != 0.0) atomicAdd(w + j, acc_head[j]);
+}
+
+__device__ __forceinline__ double gstar_sep(int pen, double v, double lambda1, double lam2, double lo, double hi)
+{
+    if (lambda1 > 0.0) {
+        if (pen == PS_PEN_L1) {
+            const double m = fmax(fabs(v) - lam2, 0.0);
+            return m * m / (2.0 * lambda1);
+        }
+        if (pen == PS_PEN_BOX) {
+            const double c = fmin(fmax(v / lambda1, lo), hi);
+            return v * c - 0.5 * lambda1 * c * c;
+        }
+        return v * v / (2.0 * lambda1);  // zero penalty
+    }
+    if (pen == PS_PEN_BOX) return fmax(v * lo, v * hi);
+    return 0.0;  // L1 (after scaling) / zero (checked through the max)
+}
+
+// separable penalties: g* partial sums and max |v_j|, v = -w / n
+__global__ void __launch_bounds__(256) k_dual_coords(const double *w, int64_t p, double inv_n, int pen,
+                                                     double lambda1, double lam2, double lo, double hi,
+                                                     double *parts, double *vmax)
+{
+    double acc = 0.0, m = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        const double v = -w[j] * inv_n;
+        acc += gstar_sep(pen, v, lambda1, lam2, lo, hi);
+        m = fmax(m, fabs(v));
+    }
+    block_sum_store(acc, parts);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(vmax, m);
+}
+
+// group penalty: per block ||v_B||, g* partial sums and the max block norm
+__global__ void __launch_bounds__(256) k_dual_blocks(const double *w, int64_t p, double inv_n, int kind, int G,
+                                                     int64_t nb, const int32_t *blk_ptr, const int32_t *blk_coords,
+                                                     double lambda1, double lam2, double *parts, double *vmax)
+{
+    double acc = 0.0, m = 0.0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        double ss = 0.0;
+        if (kind == PS_PART_GENERAL) {
+            for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; q++) {
+                const double v = w[blk_coords[q]] * inv_n;
+                ss += v * v;
+            }
+        } else {
+            const int64_t g = kind == PS_PART_SINGLETON ? 1 : G;
+            for (int64_t j = b * g; j < min((b + 1) * g, p); j++) {
+                const double v = w[j] * inv_n;
+                ss += v * v;
+            }
+        }
+        const double nrm = sqrt(ss);
+        if (lambda1 > 0.0) {
+            const double e = fmax(nrm - lam2, 0.0);
+            acc += e * e / (2.0 * lambda1);
+        }
+        m = fmax(m, nrm);
+    }
+    block_sum_store(acc, parts);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(vmax, m);
+}
+
+// lambda1 = 0 with L1 / group: conjugate sum at the scaled point c s
+template <typename VT>
+__global__ void __launch_bounds__(256) k_dual_rows_scaled(const double *s, const void *y, int64_t n, int loss,
+                                                          const double *vmax, double lam2, double *parts)
+{
+    const double c = vmax[0] > lam2 ? lam2 / vmax[0] : 1.0;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += loss_conj(loss, c * s[i], rvx<VT>(y, i));
+    block_sum_store(acc, parts);
+}
+
+// out[0] = dual value, out[1] = the dual scaling c
+__global__ void k_dual_combine(const double *sums, const double *vmax, double inv_n, double lambda1, int pen,
+                               double lam2, double *out)
+{
+    double c = 1.0;
+    if (lambda1 <= 0.0 && (pen == PS_PEN_L1 || pen == PS_PEN_GROUP) && vmax[0] > lam2) c = lam2 / vmax[0];
+    double d = -inv_n * sums[0] - sums[1];
+    if (lambda1 <= 0.0 && pen == PS_PEN_ZERO && vmax[0] > 0.0) d = -INFINITY;
+    out[0] = d;
+    out[1] = c;
+}
+
+extern "C" int ps_dual_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
+                                 int32_t x_stride, double *out, void *stream)
+{
+    if (!csr || !part || !prm || !x || !out) return ps_fail(PS_EINVAL, "null argument");
+    if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int G1 = std::max(1, sm_count() * 4);
+    const int64_t n = csr->n_rows, p = csr->n_cols;
+    double *buf = nullptr;
+    const size_t nd = (size_t)n + (size_t)p + 2 * (size_t)G1 + 4;
+    CK(pool_alloc((void **)&buf, sizeof(double) * nd, st), "ps_dual_objective alloc");
+    double *s = buf, *w = buf + n, *parts = w + p, *sums = parts + 2 * G1, *vmax = sums + 2;
+    CK(cudaMemsetAsync(w, 0, sizeof(double) * p, st), "ps_dual_objective memset");
+    CK(cudaMemsetAsync(vmax, 0, sizeof(double), st), "ps_dual_objective memset");
+    const bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+#define DUAL_ROWS(V, P) k_dual_rows<V, P><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, \
+                                                             n, prm->loss, x, x_stride, s, parts)
+    const int head = (int)std::min<int64_t>(p, DUAL_HEAD);
+    const int Gs = sm_count();  // one 512-thread CTA per SM (96 KB of head accumulators each)
+#define DUAL_SCATTER(V, P)                                                                                         \
+    do {                                                                                                         \
+        cudaFuncSetAttribute(k_dual_scatter<V, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DUAL_HEAD * 8); \
+        k_dual_scatter<V, P><<<Gs, 512, head * 8, st>>>(csr->row_ptr, csr->col_idx, csr->values, n, head, s, w); \
+    } while (0)
+    if (f64 && i64) { DUAL_ROWS(double, long long); DUAL_SCATTER(double, long long); }
+    else if (f64) { DUAL_ROWS(double, int); DUAL_SCATTER(double, int); }
+    else if (i64) { DUAL_ROWS(float, long long); DUAL_SCATTER(float, long long); }
+    else { DUAL_ROWS(float, int); DUAL_SCATTER(float, int); }
+#undef DUAL_ROWS
+#undef DUAL_SCATTER
+    const double inv_n = 1.0 / (double)n;
+    if (prm->penalty == PS_PEN_GROUP) {
+        const int64_t nb = part->kind == PS_PART_SINGLETON ? p : part->n_blocks;
+        k_dual_blocks<<<G1, 256, 0, st>>>(w, p, inv_n, part->kind, part->G, nb, part->blk_ptr, part->blk_coords,
+                                         prm->lambda1, prm->lam2, parts + G1, vmax);
+    } else {
+        k_dual_coords<<<G1, 256, 0, st>>>(w, p, inv_n, prm->penalty, prm->lambda1, prm->lam2, prm->lo, prm->hi,
+                                         parts + G1, vmax);
+    }
+    if (prm->lambda1 <= 0.0 && (prm->penalty == PS_PEN_L1 || prm->penalty == PS_PEN_GROUP)) {
+        if (f64) k_dual_rows_scaled<double><<<G1, 256, 0, st>>>(s, csr->labels, n, prm->loss, vmax, prm->lam2, parts);
+        else k_dual_rows_scaled<float><<<G1, 256, 0, st>>>(s, csr->labels, n, prm->loss, vmax, prm->lam2, parts);
+    }
+    k_finish_sum<<<1, 256, 0, st>>>(parts, G1, 2, sums, 1.0);
+    k_dual_combine<<<1, 1, 0, st>>>(sums, vmax, inv_n, prm->lambda1, prm->penalty, prm->lam2, out);
+    CK(cudaGetLastError(), "ps_dual_objective launch");
+    CK(cudaFreeAsync(buf, st), "ps_dual_objective free");
+    return PS_OK;
+}
+
 __global__ void k_sqrt(double *v) { v[0] = sqrt(v[0]); }
 
 extern "C" int ps_fixed_point_residual(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,

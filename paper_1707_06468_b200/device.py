@@ -291,7 +291,7 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self.slot_base += int(count)
 
-    def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, graph=False, **kw):
+    def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, graph=False, gap=False, **kw):
         """`total` async updates in segments of `every`; after each segment x is
         snapshotted on the device and the objective of the snapshot is evaluated
         on a side stream while the next segment runs (the reference's monitor,
@@ -306,7 +306,11 @@ class DeviceProblem:
         ~0.1 ms of host work per launch (a config-2 epoch is ~0.1 ms of GPU
         time).  Capture does not execute anything; the replay is the run.
         Worth it when the segments are short and many (bench time-to-target);
-        the capture + instantiation costs about what eager enqueueing does."""
+        the capture + instantiation costs about what eager enqueueing does.
+
+        ``gap``: also evaluate the Fenchel dual of each snapshot on the side
+        stream (ps_dual_objective) and return the duals as a fourth list
+        (duality gap = objective - dual)."""
         torch = self.torch
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device)
@@ -314,6 +318,7 @@ class DeviceProblem:
         nseg = -(-int(total) // int(every))
         snaps = [torch.empty(self.p_dev, dtype=torch.float64, device=self.device) for _ in range(min(ring, nseg))]
         outs = torch.zeros((nseg, 4), dtype=torch.float64, device=self.device)
+        douts = torch.zeros((nseg, 2), dtype=torch.float64, device=self.device) if gap else None
         ev_obj = [torch.cuda.Event() for _ in range(nseg)]
         ev_snap = [torch.cuda.Event() for _ in range(nseg)]
         stamps = torch.zeros(nseg + 1, dtype=torch.int64, device=self.device)  # %globaltimer, ns
@@ -339,6 +344,9 @@ class DeviceProblem:
                 side.wait_event(ev_snap[k])
                 _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 1,
                                           outs[k].data_ptr(), _lib.stream_ptr(side)))
+                if gap:
+                    _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), buf.data_ptr(), 1,
+                                                   douts[k].data_ptr(), _lib.stream_ptr(side)))
                 stamp(k + 1, side)
                 ev_obj[k].record(side)
             main.wait_event(ev_obj[-1])  # join the side stream
@@ -358,6 +366,8 @@ class DeviceProblem:
         objs = outs[:, :3].sum(dim=1).cpu().numpy().tolist()
         st = stamps.cpu().numpy()
         secs = [float(st[k + 1] - st[0]) / 1e9 for k in range(nseg)]
+        if gap:
+            return its, objs, secs, douts[:, 0].cpu().numpy().tolist()
         return its, objs, secs
 
     # ------------------------------------------------------------------
@@ -372,6 +382,27 @@ class DeviceProblem:
     def objective(self):
         v = self.objective_parts().cpu().numpy()
         return float(v[0] + v[1] + v[2])
+
+    def dual_objective_dev(self, x_ptr=None, stride=4, out=None, stream=None):
+        """Device tensor [D, c]: the Fenchel dual value at the dual point induced
+        by x (ps_dual_objective) and the scaling c applied to it."""
+        torch = self.torch
+        if x_ptr is None:
+            x_ptr = self.coord.data_ptr()
+        if out is None:
+            if getattr(self, "_dout", None) is None:
+                self._dout = torch.zeros(2, dtype=torch.float64, device=self.device)
+            out = self._dout
+        _lib.check(_lib.load().ps_dual_objective(self.csr, self.part, self.params(), x_ptr, stride,
+                                                 out.data_ptr(), _lib.stream_ptr(stream)))
+        return out
+
+    def duality_gap(self):
+        """(primal, dual, gap) at the current x, all evaluated on the device;
+        gap = P(x) - D(theta(x)) >= 0 and 0 exactly at the optimum."""
+        prim = self.objective()
+        dual = float(self.dual_objective_dev()[0].item())
+        return prim, dual, prim - dual
 
     def objective_parts_of(self, x):
         t = self.torch.from_numpy(self._to_stored(x)).to(self.device)
@@ -444,7 +475,7 @@ class DeviceProblem:
             other.alpha = torch.zeros_like(self.alpha)
             other.counter = torch.zeros_like(self.counter)
             other._out = torch.zeros_like(self._out)
-        for name in ("_scratch", "_side", "_grad", "_keep"):
+        for name in ("_scratch", "_side", "_grad", "_keep", "_dout"):
             if hasattr(other, name):
                 setattr(other, name, None)
         other.slot_base = 0

@@ -89,7 +89,7 @@ def run_path(lambdas, solve, rank=None, world=None):
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
                   mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0, concurrent=1,
-                  flags=0):
+                  flags=0, hot=None):
     """A ``solve(lam)`` closure over one DeviceProblem (uploaded once).
 
     ``concurrent`` > 1 (async mode): ``solve.batch(lams)`` runs that many
@@ -117,7 +117,7 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
             dp.replay(samples, gamma)
         else:
             dp.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas,
-                         warps_per_cta=warps_per_cta, flags=flags)
+                         warps_per_cta=warps_per_cta, flags=flags, hot=hot)
         parts = dp.objective_parts().cpu().numpy()
         xt = dp.field(0)  # device vector; summaries reduced on the device
         out = {"objective": float(parts.sum()), "nnz": int((xt != 0).sum().item()),
@@ -152,7 +152,7 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
                     f.lam2 = float(lam)
                     f.reset_state(stream=st)
                     f.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas_each,
-                                warps_per_cta=warps_per_cta, flags=flags, stream=st)
+                                warps_per_cta=warps_per_cta, flags=flags, hot=hot, stream=st)
                 torch.cuda.synchronize(dp.device)
                 for f, lam in zip(forks, wave):
                     parts = f.objective_parts().cpu().numpy()

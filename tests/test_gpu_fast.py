@@ -147,3 +147,20 @@ def test_fast_kernel_empty_and_ragged_rows(cuda):
     dp.run_async(80 * dp.n, gamma, seed=17)
     f = dp.objective()
     assert abs(f - fref) <= ASYNC_TOL * abs(fref), (f, fref)
+
+
+def test_checkpointed_duality_gap(cuda):
+    """run_async_checkpointed(gap=True): per-checkpoint Fenchel duals on the
+    device; the gap is nonnegative and falls with the objective gap."""
+    data = _instance(20)
+    lam = 1.0 / data.n_samples
+    dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
+                       drop_dead_blocks=True)
+    gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
+    its, objs, secs, duals = dp.run_async_checkpointed(40 * dp.n, dp.n, gamma, seed=3, graph=True, gap=True)
+    gaps = [o - d for o, d in zip(objs, duals)]
+    assert all(g >= -1e-12 for g in gaps)
+    assert gaps[-1] < 1e-3 * gaps[0]
+    assert gaps[-1] <= 1e-6 * abs(objs[-1])
+    prim, dual, gap = dp.duality_gap()
+    assert dual == pytest.approx(duals[-1], rel=1e-12)

@@ -259,3 +259,24 @@ def test_async_group_kernels_converge(cuda, name, flags, small_cases, golden_sma
     dp.run_async(epochs * n, gamma, seed=5, flags=flags)
     f = dp.objective()
     assert abs(f - fref) <= 1e-6 * abs(fref), (f, fref)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "acc_l1", "grp_random", "grp_contig", "box_sq", "zero_sq", "single_block",
+                                  "l1_ragged", "cfg2_small", "cfg5_small"])
+def test_dual_objective_matches_oracle(cuda, name, small_cases, golden_small):
+    """ps_dual_objective (device) == the oracle's numpy restatement at the
+    same x (the deterministic iterate after its replay), <= 1e-10 relative;
+    weak duality holds (gap >= 0)."""
+    from oracle import oracle as O
+
+    case = small_cases[name]
+    dp = _dp(case)
+    gamma = _gamma(case, dp)
+    n = dp.n
+    dp.replay(worker_rng(3, 0).integers(0, n, size=5 * n), gamma)
+    x = dp.x()
+    P = O.from_dataset(case["data"], case["loss"], case["penalty"], case["partition"])
+    d_ref = P.dual_objective(x)
+    prim, dual, gap = dp.duality_gap()
+    assert dual == pytest.approx(d_ref, rel=1e-10, abs=1e-13), (dual, d_ref)
+    assert gap >= -1e-12 * max(1.0, abs(prim))

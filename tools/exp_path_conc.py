@@ -13,8 +13,9 @@ lams = lp.lambda_grid(pb.group_lambda_max(d, part), 16, 1e-3)
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 ref = None
 flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+hot = (sys.argv[4] == "hot") if len(sys.argv) > 4 else None
 for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8,16").split(",")]:
-    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=K, flags=flags)
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=K, flags=flags, hot=hot)
     if K > 1:
         solve.batch(lams[:K])  # warm
     else:
