@@ -465,7 +465,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "frac_vs_spec_8TBs": achieved / 8000.0, "peak_source": peak_src,
                          "traffic_source": "profiles/ncu_traffic_r01.json (dram read+write per launch)",
                          "note": "config-2 working set (18 MB) is L2-resident: DRAM traffic << algorithmic bytes",
-                         "kernel": "sps_fast_kernel<float,int,LOGISTIC,L1,768>", "kernel_ms_avg": kavg,
+                         "kernel": "ps::sps_fast_kernel<float,int,LOGISTIC,L1,NC=1,1024>", "kernel_ms_avg": kavg,
                          "algorithmic_bytes_per_launch": bpu * total},
             "time_to_1e-6": ttt,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
