@@ -9,9 +9,16 @@
 //      (saga.py:161-163, losses.py:73-86),
 //   4. v = D (abar + lambda1 x^) + (new - alpha_i) a_i  (saga.py:164-165),
 //      z = prox_{gamma D}(x^ - gamma v)  (penalties.py:170-186),
-//   5. commits x += z - x^ (atomicAdd, asynchronous.py:104-106),
-//      alpha_i <-> new (atomicExch, :113), abar += ((new-replaced)/n) a_i
-//      (atomicAdd, :114-116).
+//   5. commits x += z - x^ (atomicAdd, asynchronous.py:104-106) -- or, when
+//      the prox returns exactly 0, stores the 0 (
+//      PS_FLAG_DELTA_ZERO keeps the literal delta) -- alpha_i <-> new
+//      (atomicExch, :113), abar += ((new-replaced)/n) a_i (atomicAdd, :114-116).
+//
+// Kernels: sps_kernel (deterministic replay + generic async, any layout),
+// sps_fast_kernel (async singleton rows <= 64 nnz: 1024-thread CTAs, a
+// three-stage row pipeline, hot columns staged per CTA in shared memory),
+// sps_group_kernel / sps_group_lane_kernel (async group lasso on contiguous
+// blocks: warp-cooperative, or one lane per block with optional staging).
 // Deterministic mode (sched->samples != NULL) replays a fixed sequence on a
 // single warp with plain stores in the exact order of sps_step
 // (saga.py:169-185): x = x^ + (z - x^), abar += (delta/n) vals, alpha_i = new.
