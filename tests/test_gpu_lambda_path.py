@@ -49,3 +49,45 @@ def test_async_path_reaches_deterministic_objectives(cuda, cfg5):
     for a, b in zip(asy, det):
         assert abs(a["objective"] - b["objective"]) <= 1e-6 * abs(b["objective"]), (a, b)
     assert det[0]["nnz"] <= det[-1]["nnz"]
+
+
+def test_forks_are_independent_states(cuda, cfg5):
+    """DeviceProblem.fork: forks share the CSR and layout but not the state.
+    Deterministic replays of different lambdas run on their own streams at
+    the same time reproduce the serial replays bitwise."""
+    import torch
+
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    lams = lp.lambda_grid(pb.group_lambda_max(d, part), 3, 1e-2)
+    solve = lp.device_solver(d, loss, part, epochs=1, mode="async")
+    dp, gamma, n = solve.problem, solve.gamma, d.n_samples
+    seq = pb.worker_rng(4, 0).integers(0, n, size=2 * n)
+    serial = []
+    for lam in lams:
+        dp.lam2 = lam
+        dp.reset_state()
+        dp.replay(seq, gamma)
+        serial.append(dp.x())
+    forks = [dp] + [dp.fork() for _ in range(len(lams) - 1)]
+    streams = [torch.cuda.Stream() for _ in forks]
+    s_dev = torch.from_numpy(seq).to(dp.device)
+    for f, st, lam in zip(forks, streams, lams):
+        f.lam2 = lam
+        f.reset_state(stream=st)
+        f.replay(s_dev, gamma, stream=st)
+    torch.cuda.synchronize()
+    for f, x in zip(forks, serial):
+        assert np.array_equal(f.x(), x)
+    assert forks[1].coord.data_ptr() != forks[0].coord.data_ptr()
+    assert forks[1].col.data_ptr() == forks[0].col.data_ptr()  # CSR shared
+
+
+def test_concurrent_path_matches_serial_objectives(cuda, cfg5):
+    """The concurrent schedule (forks on streams, lane kernel) and the serial
+    one agree on every lambda's objective after the same epochs to 1e-6."""
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    lams = lp.lambda_grid(pb.group_lambda_max(d, part), 6, 1e-1)
+    serial = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="async"))
+    conc = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="async", concurrent=6))
+    for a, b in zip(serial, conc):
+        assert b["objective"] == pytest.approx(a["objective"], rel=1e-6), (a["lam"], a["objective"], b["objective"])
