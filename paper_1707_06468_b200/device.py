@@ -50,7 +50,7 @@ class DeviceProblem:
     """
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
-                 value_dtype="auto", hot_max=512, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
+                 value_dtype="auto", hot_max=None, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
                  _labels=None, _device_csr=None, _shape=None):
         torch = _torch()
         _lib.require_device()
@@ -109,6 +109,12 @@ class DeviceProblem:
             self._setup_partition(partition)
             self.H, self.hot_shift, self.perm, self.perm_np, self.p_dev = 0, 0, None, None, self.p
             self.hot_unit = 1 if self.part_kind == "singleton" else int(self.part.G)
+            if hot_max is None:
+                # staged columns: 512, or 1024 when the coordinate records (32 B each)
+                # do not fit in L2 -- then every staged column saves HBM round trips,
+                # not just L2 ones (config 3: 1.31 -> 1.69 G updates/s; config 2 and
+                # 4, whose records are L2-resident, gain nothing from 1024)
+                hot_max = 1024 if 32 * self.p > 96 * (1 << 20) else 512
             if self.part_kind in ("singleton", "contiguous") and hot_max > 0 and self.n >= hot_min_rows:
                 # hot_max columns (singleton), or whole blocks up to 1024 staged coordinates
                 units = hot_max if self.hot_unit == 1 else max(1, min(4 * hot_max, 1024) // self.hot_unit)
