@@ -7,8 +7,9 @@ sys.path.insert(0, str(ROOT))
 import paper_1707_06468_b200 as pb
 from paper_1707_06468_b200 import problems
 which = int(sys.argv[1])
+mf = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0 / 512
 for hm in [int(x) for x in sys.argv[2].split(",")]:
-    c = problems.config3(hot_max=hm) if which == 3 else problems.config4(hot_max=hm)
+    c = problems.config3(hot_max=hm, hot_min_frac=mf) if which == 3 else problems.config4(hot_max=hm, hot_min_frac=mf)
     dp = c["problem"]
     gamma = pb.resolve_step_size("1/2L", dp.L, dp.n, c["loss"].lambda1)
     dp.reset_state()
