@@ -18,8 +18,10 @@ gamma = pb.resolve_step_size("1/2L", dp.L, n, cfg["loss"].lambda1)
 fstar = json.loads((ROOT / "tests/golden/cfg2_fstar.json").read_text())["fstar"]
 grid = sys.argv[1] if len(sys.argv) > 1 else "32:24:4,32:24:6,32:16:4,24:16:4,24:16:6,32:32:6"
 for g in grid.split(","):
-    wpc, hp, c = g.split(":")
-    kw = dict(warps_per_cta=int(wpc), hot_period=int(hp), contention=float(c))
+    f = g.split(":")
+    wpc, hp, c = f[0], f[1], f[2]
+    kw = dict(warps_per_cta=int(wpc), hot_period=int(hp), contention=float(c),
+              flags=int(f[3]) if len(f) > 3 else 0)
     dp.reset_state(); dp.run_async_checkpointed(2 * n, n, gamma, seed=3, **kw)  # warm
     tt = []
     for r in range(3):
@@ -34,5 +36,5 @@ for g in grid.split(","):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(); dp.run_async(30 * n, gamma, seed=50 + r, **kw); e.record(); torch.cuda.synchronize()
         ms.append(s.elapsed_time(e))
-    print(json.dumps({"wpc": wpc, "hp": hp, "c": c, "ttt_ms_epochs": [(round(a * 1e3, 3) if a else None, b) for a, b in tt],
+    print(json.dumps({"wpc": wpc, "hp": hp, "c": c, "flags": kw["flags"], "ttt_ms_epochs": [(round(a * 1e3, 3) if a else None, b) for a, b in tt],
                       "solve_Mups": round(30 * n / np.mean(ms) / 1e3, 1)}), flush=True)
