@@ -304,12 +304,15 @@ def main():
     import torch
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
+    # one GPU per rank; BENCH_DIST_BACKEND=gloo with fewer GPUs than ranks is
+    # only a functional dry run of the multi-rank path (ranks never wait on
+    # each other on the device: no data-path collective)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
     import paper_1707_06468_b200 as pb
 
     cfg = workload(rank)
