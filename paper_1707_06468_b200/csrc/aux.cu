@@ -306,48 +306,44 @@ extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, p
 }
 
 // ---------------------------------------------------------------------------
-// objective: warp per row (grid-stride), then p-coordinate terms.
-template <typename VT, typename PT>
-__global__ void __launch_bounds__(256) k_loss_sum(const void *row_ptr, const int32_t *col, const void *val,
-                                                  const void *y, int64_t n, int loss, const double *x, int xs,
-                                                  double *parts)
+// ps_objective (losses.py:134-136: mean loss + lambda1/2 ||x||^2 + penalty) in
+// one launch (checkpoints evaluate it every epoch; separate launches for the
+// loss pass, the coordinate terms, the final sum and the combine cost more
+// than the work): per-CTA partials of the loss (thread per row for short rows,
+// warp per row otherwise), of ||x||^2 and of the penalty (|x|, box violations,
+// or sum_B ||x_B|| for the group penalty, penalties.py:97-101), then the last
+// CTA to finish sums them in a fixed order (deterministic) and combines.
+template <typename VT, typename PT, bool TROW>
+__global__ void __launch_bounds__(256) k_objective_fused(const void *row_ptr, const int32_t *col, const void *val,
+                                                         const void *y, int64_t n, int loss, const double *x, int xs,
+                                                         int64_t p, int pen, double lo, double hi, int kind, int G,
+                                                         int64_t nb, const int32_t *blk_ptr, const int32_t *blk_coords,
+                                                         double lambda1, double lam2, double *parts, unsigned *done,
+                                                         double *out)
 {
-    int lane = threadIdx.x & 31;
-    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int G1 = gridDim.x;
     double acc = 0.0;
-    for (int64_t i = w; i < n; i += nw) {
-        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
-        double z = 0.0;
-        for (int64_t e = lo + lane; e < hi; e += 32) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
-        z = warp_sum(z);
-        if (lane == 0) acc += loss_value(loss, z, rvx<VT>(y, i));
-    }
-    block_sum_store(acc, parts);
-}
-
-// thread per row (rows of <= 64 nonzeros): the row's gathers are independent
-// loads in flight together; one loss evaluation per thread.
-template <typename VT, typename PT>
-__global__ void __launch_bounds__(256) k_loss_sum_t(const void *row_ptr, const int32_t *col, const void *val,
-                                                    const void *y, int64_t n, int loss, const double *x, int xs,
-                                                    double *parts)
-{
-    double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
-        double z = 0.0;
+    if (TROW) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            int64_t lo_ = rpx<PT>(row_ptr, i), hi_ = rpx<PT>(row_ptr, i + 1);
+            double z = 0.0;
 #pragma unroll 8
-        for (int64_t e = lo; e < hi; e++) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
-        acc += loss_value(loss, z, rvx<VT>(y, i));
+            for (int64_t e = lo_; e < hi_; e++) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+            acc += loss_value(loss, z, rvx<VT>(y, i));
+        }
+    } else {
+        const int lane = threadIdx.x & 31;
+        const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        for (int64_t i = w; i < n; i += nw) {
+            int64_t lo_ = rpx<PT>(row_ptr, i), hi_ = rpx<PT>(row_ptr, i + 1);
+            double z = 0.0;
+            for (int64_t e = lo_ + lane; e < hi_; e += 32) z += rvx<VT>(val, e) * x[(int64_t)col[e] * xs];
+            z = warp_sum(z);
+            if (lane == 0) acc += loss_value(loss, z, rvx<VT>(y, i));
+        }
     }
     block_sum_store(acc, parts);
-}
-
-// ||x||^2, penalty partial sums (L1 |x|, box violations) per CTA.
-__global__ void __launch_bounds__(256) k_coord_terms(const double *x, int xs, int64_t p, int pen, double lo,
-                                                     double hi, double *parts_xx, double *parts_pen)
-{
     double xx = 0.0, pv = 0.0;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
         double v = x[j * xs];
@@ -355,43 +351,58 @@ __global__ void __launch_bounds__(256) k_coord_terms(const double *x, int xs, in
         if (pen == PS_PEN_L1) pv += fabs(v);
         else if (pen == PS_PEN_BOX && !(v >= lo && v <= hi)) pv += 1.0;
     }
-    block_sum_store(xx, parts_xx);
-    block_sum_store(pv, parts_pen);
-}
-
-// group value (penalties.py:97-101): sum_B ||x_B||_2.
-__global__ void __launch_bounds__(256) k_group_value(const double *x, int xs, int64_t p, int kind, int G,
-                                                     int64_t nb, const int32_t *blk_ptr, const int32_t *blk_coords,
-                                                     double *parts)
-{
-    double acc = 0.0;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-        double ss = 0.0;
-        if (kind == PS_PART_GENERAL) {
-            for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; q++) {
-                double v = x[(int64_t)blk_coords[q] * xs];
-                ss += v * v;
+    block_sum_store(xx, parts + G1);
+    if (pen == PS_PEN_GROUP) {
+        double gv = 0.0;
+        for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+            double ss = 0.0;
+            if (kind == PS_PART_GENERAL) {
+                for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; q++) {
+                    double v = x[(int64_t)blk_coords[q] * xs];
+                    ss += v * v;
+                }
+            } else {
+                int64_t g = kind == PS_PART_SINGLETON ? 1 : G;
+                for (int64_t j = b * g; j < min((b + 1) * g, p); j++) {
+                    double v = x[j * xs];
+                    ss += v * v;
+                }
             }
-        } else {
-            int64_t g = kind == PS_PART_SINGLETON ? 1 : G;
-            for (int64_t j = b * g; j < min((b + 1) * g, p); j++) {
-                double v = x[j * xs];
-                ss += v * v;
-            }
+            gv += sqrt(ss);
         }
-        acc += sqrt(ss);
+        block_sum_store(gv, parts + 2 * G1);
+    } else {
+        block_sum_store(pv, parts + 2 * G1);
     }
-    block_sum_store(acc, parts);
-}
-
-__global__ void k_objective_combine(const double *sums, double lambda1, int pen, double lam2, double *out)
-{
-    // sums: [loss_sum/n, xx, penraw]
-    out[0] = sums[0];
-    out[1] = 0.5 * lambda1 * sums[1];
-    if (pen == PS_PEN_L1 || pen == PS_PEN_GROUP) out[2] = lam2 * sums[2];
-    else if (pen == PS_PEN_BOX) out[2] = sums[2] > 0 ? INFINITY : 0.0;
-    else out[2] = 0.0;
+    // last CTA: fixed-order final sums + combine
+    __shared__ bool last;
+    __threadfence();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == (unsigned)gridDim.x - 1u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ double sums[3];
+    for (int c = 0; c < 3; c++) {
+        double v = 0.0;
+        for (int q = threadIdx.x; q < G1; q += blockDim.x) v += ld_cg(parts + (int64_t)c * G1 + q);
+        __shared__ double red[8];
+        v = warp_sum(v);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+            sums[c] = c == 0 ? t * (1.0 / (double)n) : t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = sums[0];
+        out[1] = 0.5 * lambda1 * sums[1];
+        if (pen == PS_PEN_L1 || pen == PS_PEN_GROUP) out[2] = lam2 * sums[2];
+        else if (pen == PS_PEN_BOX) out[2] = sums[2] > 0 ? INFINITY : 0.0;
+        else out[2] = 0.0;
+    }
 }
 
 extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
@@ -402,27 +413,30 @@ extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps
     cudaStream_t st = (cudaStream_t)stream;
     const int G1 = std::max(1, sm_count() * 4);  // CTAs per partial pass (fixed -> deterministic)
     double *parts = nullptr;
-    CK(pool_alloc((void **)&parts, sizeof(double) * (3 * G1 + 3), st), "ps_objective alloc");
-    double *sums = parts + 3 * G1;
-    int64_t n = csr->n_rows, p = csr->n_cols;
-    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (part->max_row_nnz > 0 && part->max_row_nnz <= 64) {  // short rows: thread per row
-        if (f64 && i64) k_loss_sum_t<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-        else if (f64) k_loss_sum_t<double, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-        else if (i64) k_loss_sum_t<float, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-        else k_loss_sum_t<float, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-    } else if (f64 && i64) k_loss_sum<double, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-    else if (f64) k_loss_sum<double, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-    else if (i64) k_loss_sum<float, long long><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-    else k_loss_sum<float, int><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n, prm->loss, x, x_stride, parts);
-    k_coord_terms<<<G1, 256, 0, st>>>(x, x_stride, p, prm->penalty, prm->lo, prm->hi, parts + G1, parts + 2 * G1);
-    if (prm->penalty == PS_PEN_GROUP) {
-        int64_t nb = part->kind == PS_PART_SINGLETON ? p : part->n_blocks;
-        k_group_value<<<G1, 256, 0, st>>>(x, x_stride, p, part->kind, part->G, nb, part->blk_ptr, part->blk_coords,
-                                          parts + 2 * G1);
+    CK(pool_alloc((void **)&parts, sizeof(double) * (3 * G1 + 1), st), "ps_objective alloc");
+    unsigned *done = reinterpret_cast<unsigned *>(parts + 3 * G1);
+    CK(cudaMemsetAsync(done, 0, sizeof(unsigned), st), "ps_objective memset");
+    const int64_t n = csr->n_rows, p = csr->n_cols;
+    const bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    const bool trow = part->max_row_nnz > 0 && part->max_row_nnz <= 64;  // short rows: thread per row
+    const int64_t nb = part->kind == PS_PART_SINGLETON ? p : part->n_blocks;
+#define OBJ_FUSED(V, P, T)                                                                                           \
+    k_objective_fused<V, P, T><<<G1, 256, 0, st>>>(csr->row_ptr, csr->col_idx, csr->values, csr->labels, n,        \
+                                                   prm->loss, x, x_stride, p, prm->penalty, prm->lo, prm->hi,      \
+                                                   part->kind, part->G, nb, part->blk_ptr, part->blk_coords,       \
+                                                   prm->lambda1, prm->lam2, parts, done, out)
+    if (trow) {
+        if (f64 && i64) OBJ_FUSED(double, long long, true);
+        else if (f64) OBJ_FUSED(double, int, true);
+        else if (i64) OBJ_FUSED(float, long long, true);
+        else OBJ_FUSED(float, int, true);
+    } else {
+        if (f64 && i64) OBJ_FUSED(double, long long, false);
+        else if (f64) OBJ_FUSED(double, int, false);
+        else if (i64) OBJ_FUSED(float, long long, false);
+        else OBJ_FUSED(float, int, false);
     }
-    k_finish_sum<<<1, 256, 0, st>>>(parts, G1, 3, sums, 1.0 / (double)n);
-    k_objective_combine<<<1, 1, 0, st>>>(sums, prm->lambda1, prm->penalty, prm->lam2, out);
+#undef OBJ_FUSED
     CK(cudaGetLastError(), "ps_objective launch");
     CK(cudaFreeAsync(parts, st), "ps_objective free");
     return PS_OK;
