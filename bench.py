@@ -246,41 +246,56 @@ def big_config_bench(which, peak):
     return out
 
 
-def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
-    """Solve from zero with an objective checkpoint every epoch.  Checkpoints
-    are pipelined on the device (DeviceProblem.run_async_checkpointed: x
-    snapshot + objective on a side stream while the next epoch runs); the time
-    of a checkpoint is when its objective is known (CUDA events, evaluations
-    included).  Log-linear interpolation of the first crossing
-    (asynchronous.py:213-230) on the RELATIVE gap (F - F*)/|F*|."""
+def _first_crossing(its, walls, rel, n, target):
+    """Log-linear interpolation of the first crossing (asynchronous.py:213-230)
+    on the RELATIVE gap; returns (seconds, epochs) or None."""
     import math
 
-    dp.reset_state()  # untimed warm-up of the checkpointed path (side stream, objective kernels)
-    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, ctas=ctas, warps_per_cta=wpc, graph=True, gap=True)
-    dp.reset_state()
-    # the 30 epochs + checkpoints as one CUDA graph (captured, then replayed and timed on the device)
-    its, objs, walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc,
-                                                 graph=True)
-    # the same solve with the Fenchel dual (duality gap) also evaluated at every checkpoint
-    dp.reset_state()
-    _, gobjs, gwalls, duals = dp.run_async_checkpointed(total, n, gamma, seed=seed, ctas=ctas, warps_per_cta=wpc,
-                                                        graph=True, gap=True)
-    rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
-    hit = None
     prev_rel, prev_w, prev_it = 1.0, 0.0, 0
     for it, w, r in zip(its, walls, rel):
         if r <= target:
             frac = math.log(prev_rel / target) / math.log(prev_rel / r) if prev_rel > r else 1.0
-            hit = (prev_w + frac * (w - prev_w), (prev_it + frac * (it - prev_it)) / n)
-            break
+            return prev_w + frac * (w - prev_w), (prev_it + frac * (it - prev_it)) / n
         prev_rel, prev_w, prev_it = r, w, it
+    return None
+
+
+def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
+    """Solve from zero in ONE launch with the reference's live monitor
+    (asynchronous.py:181-198; DeviceProblem.run_async_monitored): every epoch
+    mark the running solve's coordinate records are snapshotted by a
+    copy-engine DMA (inconsistent, as the reference's snapshot_x) and its
+    objective evaluated afterwards; a checkpoint's time is its snapshot's
+    device time + one measured objective evaluation (evals
+    included).  Log-linear interpolation of the first crossing on the
+    RELATIVE gap (F - F*)/|F*|.  Also reported: the stop-the-world schedule
+    (one launch per epoch, checkpoints between launches, one CUDA graph) and
+    the duality gap of every monitored checkpoint."""
+    mon = dict(ctas=ctas, warps_per_cta=wpc)
+    dp.reset_state()  # untimed warm-up of both paths
+    dp.run_async_monitored(2 * n, n, gamma, seed=seed + 1, **mon)
+    dp.reset_state()
+    dp.run_async_checkpointed(2 * n, n, gamma, seed=seed + 1, graph=True, **mon)
+    dp.reset_state()
+    its, objs, walls, duals = dp.run_async_monitored(total, n, gamma, seed=seed, gap=True, **mon)
+    rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
+    hit = _first_crossing(its[1:], walls[1:], rel[1:], n, target)
+    dp.reset_state()
+    g_its, g_objs, g_walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, graph=True, **mon)
+    g_rel = [max((o - fstar) / abs(fstar), 1e-300) for o in g_objs]
+    g_hit = _first_crossing(g_its, g_walls, g_rel, n, target)
     return {"target_rel_gap": target, "seconds": hit[0] if hit else None, "epochs": hit[1] if hit else None,
             "reached": hit is not None, "final_rel_gap": rel[-1], "epochs_run": total / n,
             "fstar": fstar, "wall_incl_evals_s": walls[-1],
-            "duality_gap": {"final": gobjs[-1] - duals[-1],
-                            "rel_per_epoch": [float(f"{(o - d) / abs(o):.3e}") for o, d in zip(gobjs, duals)],
-                            "seconds_with_gap_checkpoints": gwalls[-1]}, "checkpoints": "every epoch, pipelined on a side stream, whole sequence replayed as one CUDA graph; "
-                           "times = device %globaltimer stamps after each checkpoint objective"}
+            "checkpoints": "the reference's live monitor: one launch, a copy-engine snapshot of the running solve "
+                           "at every epoch mark (ps_run_monitored), objective evaluated per snapshot; time = "
+                           "snapshot device time + one measured objective evaluation",
+            "checkpoint_epochs": [round(i / n, 3) for i in its],
+            "stop_the_world": {"seconds": g_hit[0] if g_hit else None, "epochs": g_hit[1] if g_hit else None,
+                               "schedule": "one launch per epoch, snapshot + objective between launches, "
+                                           "replayed as one CUDA graph"},
+            "duality_gap": {"final": objs[-1] - duals[-1],
+                            "rel_per_checkpoint": [float(f"{(o - d) / abs(o):.3e}") for o, d in zip(objs, duals)]}}
 
 
 def main():

@@ -199,6 +199,18 @@ int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_inout, int3
 int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned long long *counter,
                    void *stream);
 
+/* One asynchronous ps_run with the reference's live monitor
+ * (asynchronous.py:181-198): this call blocks, polls sched->counter and, each
+ * time it crosses a multiple of `every`, copies the live coordinate records
+ * (p x 4 doubles, an inconsistent snapshot while the warps keep updating) into
+ * snaps[k] (pinned HOST memory: a copy-engine DMA beside the kernel).  snaps[0] is the state before the first update,
+ * the last one the state after the launch; snap_counts / snap_ms (host) get
+ * the counter value and the device time (ms since the launch) of each;
+ * *n_snaps <= max_snaps.  The solve never stops for a checkpoint. */
+int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
+                     double *alpha, const ps_sched_t *sched, void *scratch, void *stream, int64_t every,
+                     int32_t max_snaps, double *snaps, int64_t *snap_counts, float *snap_ms, int32_t *n_snaps);
+
 /* Fenchel dual objective at the dual point induced by x (theta_i = -l'(a_i.x, b_i)):
  * out[0] = D, out[1] = the scaling applied to theta (lambda1 = 0 with L1 / group,
  * else 1); duality gap = ps_objective - D >= 0.  No reference counterpart (the

@@ -33,6 +33,8 @@
 //   GENERAL    any BlockPartition; T_i / slot positions precomputed by
 //              ps_prepare; blocks processed one at a time.
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 
 #include "common.cuh"
@@ -187,6 +189,7 @@ __device__ __forceinline__ void drop_pending_x(const HotView &h, int s)
 constexpr int HOT_PER_LANE = 32;  // H <= 1024 (dirty bitmask: one 32-bit word per lane)
 constexpr int HOT_MAX = 32 * HOT_PER_LANE;
 constexpr int HOT_TIER0 = 128;  // slots refreshed on every flush
+constexpr int PROGRESS_BATCH = 16;  // fast kernel: updates per progress-counter bump
 
 // global coordinate of hot slot s: unit s / U stored at unit (s / U) << hot_shift
 __device__ __forceinline__ int64_t hot_coord(const KArgs &a, int s)
@@ -959,6 +962,10 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                 hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
                 until_flush = a.period;
             }
+            // progress counter, bumped every PROGRESS_BATCH updates (the workers'
+            // counter_batch, asynchronous.py:155-162): a host monitor reads it
+            if (lane == 0 && (slot - first) % PROGRESS_BATCH == 0)
+                atomicAdd(a.counter, (unsigned long long)PROGRESS_BATCH);
             if (!more) break;
             cur = nxt;
         }
@@ -977,8 +984,8 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         }
     }
     if (lane == 0) {
-        int64_t mine = q + (gw < rr ? 1 : 0);
-        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
+        const int64_t mine = q + (gw < rr ? 1 : 0);
+        if (mine % PROGRESS_BATCH) atomicAdd(a.counter, (unsigned long long)(mine % PROGRESS_BATCH));
     }
     if (a.H > 0) {
         hot_async_drain();
@@ -1723,5 +1730,110 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     void *args[] = {(void *)&a};
     cudaError_t e = cudaLaunchKernel(L.kernel, dim3(L.ctas), dim3(L.wpc * 32), args, L.smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run launch");
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ps_run_monitored: the reference's monitor (asynchronous.py:187-198) on the
+// device.  One asynchronous launch runs the whole solve; this (host) thread
+// polls the progress counter and, each time it crosses a checkpoint mark,
+// snapshots the live coordinate records into (pinned) host memory on a copy
+// stream -- a copy-engine DMA that runs beside the kernel (a device-to-device
+// memcpy would need SMs and wait for the launch), i.e. an inconsistent
+// snapshot taken while the warps keep updating, as snapshot_x
+// (asynchronous.py:65-66) is -- and records an event after it.  The solve
+// never stops for a checkpoint.  Objectives of the snapshots are evaluated by
+// the caller afterwards (ps_objective, stride 4).
+extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
+                                double *alpha, const ps_sched_t *sched, void *scratch, void *stream, int64_t every,
+                                int32_t max_snaps, double *snaps, int64_t *snap_counts, float *snap_ms,
+                                int32_t *n_snaps)
+{
+    if (!sched || !snaps || !snap_counts || !snap_ms || !n_snaps || every < 1 || max_snaps < 1)
+        return ps_fail(PS_EINVAL, "bad monitor arguments");
+    if (sched->samples) return ps_fail(PS_EINVAL, "the monitor is for asynchronous runs");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t p = csr->n_cols, total = sched->count;
+    // per-device monitor resources, created once and kept: copy + poll streams,
+    // a pinned counter mirror, a growing pool of events
+    struct Mon {
+        cudaStream_t cp = nullptr, poll = nullptr;
+        unsigned long long *h_cnt = nullptr;
+        cudaEvent_t ev0 = nullptr;
+        std::vector<cudaEvent_t> evs;
+    };
+    static Mon mons[64];
+    static std::mutex locks[64];  // one monitored run per device at a time (shared resources)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return ps_fail(PS_EINVAL, "device index out of range");
+    std::lock_guard<std::mutex> guard(locks[dev]);
+    Mon &m = mons[dev];
+    int rc = PS_OK;
+#define MCK(x, what)                                       \
+    do {                                                   \
+        cudaError_t e_ = (x);                              \
+        if (e_ != cudaSuccess) {                           \
+            rc = ps_cuda_fail(e_, what);                   \
+            return rc;                                     \
+        }                                                  \
+    } while (0)
+    if (!m.cp) {
+        MCK(cudaStreamCreateWithFlags(&m.cp, cudaStreamNonBlocking), "monitor stream");
+        MCK(cudaStreamCreateWithFlags(&m.poll, cudaStreamNonBlocking), "monitor stream");
+        MCK(cudaMallocHost((void **)&m.h_cnt, sizeof(unsigned long long)), "monitor pinned counter");
+        MCK(cudaEventCreate(&m.ev0), "monitor event");
+    }
+    while ((int)m.evs.size() < max_snaps) {
+        cudaEvent_t e;
+        MCK(cudaEventCreate(&e), "monitor event");
+        m.evs.push_back(e);
+    }
+    cudaStream_t cp = m.cp, poll = m.poll;
+    cudaEvent_t ev0 = m.ev0;
+    std::vector<cudaEvent_t> &evs = m.evs;
+    unsigned long long *h_cnt = m.h_cnt;
+    MCK(cudaMemsetAsync(sched->counter, 0, sizeof(unsigned long long), st), "monitor counter reset");
+    MCK(cudaEventRecord(ev0, st), "monitor event");
+    // checkpoint 0: the state before the first update (asynchronous.py:181)
+    int ns = 0;
+    MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
+    MCK(cudaMemcpyAsync(snaps, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, cp), "monitor snapshot");
+    MCK(cudaEventRecord(evs[0], cp), "monitor event");
+    snap_counts[0] = 0;
+    ns = 1;
+    // the solve must not start before snapshot 0 is taken
+    MCK(cudaStreamWaitEvent(st, evs[0], 0), "monitor wait");
+    int r = ps_run(csr, part, prm, coord, alpha, sched, scratch, stream);
+    if (r) return r;
+    int64_t next_mark = every;
+    while (true) {
+        const bool done = cudaStreamQuery(st) == cudaSuccess;
+        if (done) break;
+        MCK(cudaMemcpyAsync(h_cnt, sched->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, poll),
+            "monitor poll");
+        MCK(cudaStreamSynchronize(poll), "monitor poll");
+        const int64_t c = (int64_t)*h_cnt;
+        if (c >= next_mark && next_mark < total && ns < max_snaps - 1) {
+            MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost,
+                                cp),
+                "monitor snapshot");
+            MCK(cudaEventRecord(evs[ns], cp), "monitor event");
+            snap_counts[ns++] = c;
+            while (next_mark <= c) next_mark += every;
+        }
+    }
+    // final checkpoint: after the launch (consistent)
+    MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
+    MCK(cudaStreamSynchronize(st), "monitor join");
+    MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, st),
+        "monitor snapshot");
+    MCK(cudaEventRecord(evs[ns], st), "monitor event");
+    snap_counts[ns++] = total;
+    MCK(cudaStreamSynchronize(st), "monitor join");
+    MCK(cudaStreamSynchronize(cp), "monitor join");
+    for (int k = 0; k < ns; k++) MCK(cudaEventElapsedTime(snap_ms + k, ev0, evs[k]), "monitor timing");
+    *n_snaps = ns;
+#undef MCK
     return PS_OK;
 }

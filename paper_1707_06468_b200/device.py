@@ -297,6 +297,58 @@ class DeviceProblem:
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
         self.slot_base += int(count)
 
+    def run_async_monitored(self, total, every, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=4.0,
+                            hot=None, hot_period=0, flags=0, gap=False):
+        """`total` lock-free updates in ONE launch with the reference's live
+        monitor (asynchronous.py:181-198, ps_run_monitored): each time the
+        progress counter crosses a multiple of `every`, the live coordinate
+        records are copied (an inconsistent snapshot, as snapshot_x is) while
+        the warps keep going.  The objectives (and with ``gap`` the Fenchel
+        duals) of the snapshots are evaluated afterwards; a checkpoint's time is
+        its snapshot's device time plus one measured objective evaluation (the
+        time the monitor would need to know it).  Returns (iterations,
+        objectives, seconds[, duals])."""
+        torch = self.torch
+        if hot is None:
+            hot = self.part_kind == "singleton"
+        nmax = int(-(-int(total) // int(every))) + 2
+        sched = self._sched(total, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta,
+                            contention=contention, hot=hot, hot_period=hot_period, flags=flags)
+        scr = self._scratch_for(sched)
+        snaps = torch.empty((nmax, self.p_dev, 4), dtype=torch.float64, pin_memory=True)  # DMA targets
+        counts = (ctypes.c_int64 * nmax)()
+        ms = (ctypes.c_float * nmax)()
+        ns = ctypes.c_int32(0)
+        L = _lib.load()
+        _lib.check(L.ps_run_monitored(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
+                                      self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(), int(every), nmax,
+                                      snaps.data_ptr(), counts, ms, ctypes.byref(ns)))
+        self.slot_base += int(total)
+        k = ns.value
+        outs = torch.zeros((k, 4), dtype=torch.float64, device=self.device)
+        duals = torch.zeros((k, 2), dtype=torch.float64, device=self.device) if gap else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        buf = torch.empty((self.p_dev, 4), dtype=torch.float64, device=self.device)
+        for j in range(k):
+            buf.copy_(snaps[j])
+            if j == 1:
+                e0.record()
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 4,
+                                      outs[j].data_ptr(), _lib.stream_ptr()))
+            if j == 1:
+                e1.record()
+            if gap:
+                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), buf.data_ptr(), 4,
+                                               duals[j].data_ptr(), _lib.stream_ptr()))
+        torch.cuda.synchronize(self.device)
+        t_eval = e0.elapsed_time(e1) / 1e3 if k > 1 else 0.0
+        objs = outs[:, :3].sum(dim=1).cpu().numpy().tolist()
+        its = [int(counts[j]) for j in range(k)]
+        secs = [float(ms[j]) / 1e3 + (t_eval if j > 0 else 0.0) for j in range(k)]
+        if gap:
+            return its, objs, secs, duals[:, 0].cpu().numpy().tolist()
+        return its, objs, secs
+
     def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, graph=False, gap=False, **kw):
         """`total` async updates in segments of `every`; after each segment x is
         snapshotted on the device and the objective of the snapshot is evaluated

@@ -164,3 +164,38 @@ def test_checkpointed_duality_gap(cuda):
     assert gaps[-1] <= 1e-6 * abs(objs[-1])
     prim, dual, gap = dp.duality_gap()
     assert dual == pytest.approx(duals[-1], rel=1e-12)
+
+
+def test_live_monitor_checkpoints(cuda):
+    """run_async_monitored (ps_run_monitored): one launch, snapshots of the
+    running solve at the epoch marks; counters and device times increase,
+    the first checkpoint is x0, the last the state after the launch, and the
+    solve reaches the optimum; the final objective equals the live one."""
+    data = _instance(20)
+    lam = 1.0 / data.n_samples
+    dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
+                       drop_dead_blocks=True)
+    gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
+    fref = _fstar(dp, gamma)
+    its, objs, secs, duals = dp.run_async_monitored(60 * dp.n, dp.n, gamma, seed=3, gap=True)
+    assert its[0] == 0 and its[-1] == 60 * dp.n and len(its) >= 3
+    assert all(b >= a for a, b in zip(its, its[1:]))
+    assert all(b >= a for a, b in zip(secs[1:], secs[2:]))
+    assert objs[0] == pytest.approx(np.log(2.0), rel=1e-12)  # x0 = 0
+    assert objs[-1] == pytest.approx(dp.objective(), rel=1e-14)
+    assert abs(objs[-1] - fref) <= ASYNC_TOL * abs(fref)
+    assert all(o - d >= -1e-12 for o, d in zip(objs, duals))
+    assert dp.slot_base == 60 * dp.n
+
+
+def test_run_async_api_uses_the_live_monitor(cuda):
+    """pb.run_async with threads > 1: trace rows from the live monitor."""
+    data = _instance(20)
+    lam = 1.0 / data.n_samples
+    part = pb.singleton_partition(data.n_features)
+    idx = pb.build_support_index(data.features, part, drop_dead_blocks=True)
+    tr = pb.run_async(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), part,
+                      pb.AsyncConfig(epochs=20, seed=1, threads=4), index=idx)
+    assert tr.iterations[0] == 0 and tr.iterations[-1] == 20 * data.n_samples
+    assert all(b >= a for a, b in zip(tr.iterations, tr.iterations[1:]))
+    assert len(tr.objective) >= 3 and tr.objective[-1] < tr.objective[0]
