@@ -234,13 +234,14 @@ def big_config_bench(which, peak):
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
-    f1 = dp.objective()
+    f1, d1, gap1 = dp.duality_gap()  # certified: F(x) - F* <= gap
     bpu = dp.bytes_per_update()
     ups = total / (ms / 1e3)
     out = {"workload": c["name"] + f", {c['epochs']} async epochs from x0=0 in one launch, device-generated (K7)",
            "n": dp.n, "p": dp.p, "nnz": dp.nnz, "value": ups, "unit": UNIT, "kernel_ms": ms,
            "bytes_per_update": bpu, "achieved_GBps": bpu * ups / 1e9, "roofline_frac": bpu * ups / 1e9 / peak,
-           "objective_start": f0, "objective_end": f1, "hot_columns": dp.H}
+           "objective_start": f0, "objective_end": f1, "duality_gap_end": gap1,
+           "certified_rel_suboptimality_end": gap1 / abs(f1), "hot_columns": dp.H}
     del dp, c
     torch.cuda.empty_cache()
     return out
@@ -280,6 +281,9 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
     its, objs, walls, duals = dp.run_async_monitored(total, n, gamma, seed=seed, gap=True, **mon)
     rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
     hit = _first_crossing(its[1:], walls[1:], rel[1:], n, target)
+    # certified by the duality gap alone (no F* needed): (F - D)/|F| <= target
+    crel = [max((o - d) / abs(o), 1e-300) for o, d in zip(objs, duals)]
+    chit = _first_crossing(its[1:], walls[1:], crel[1:], n, target)
     dp.reset_state()
     g_its, g_objs, g_walls = dp.run_async_checkpointed(total, n, gamma, seed=seed, graph=True, **mon)
     g_rel = [max((o - fstar) / abs(fstar), 1e-300) for o in g_objs]
@@ -295,6 +299,8 @@ def time_to_target(dp, gamma, total, n, fstar, seed, ctas, wpc, target=1e-6):
                                "schedule": "one launch per epoch, snapshot + objective between launches, "
                                            "replayed as one CUDA graph"},
             "duality_gap": {"final": objs[-1] - duals[-1],
+                            "certified_seconds": chit[0] if chit else None,
+                            "certified_epochs": chit[1] if chit else None,
                             "rel_per_checkpoint": [float(f"{(o - d) / abs(o):.3e}") for o, d in zip(objs, duals)]}}
 
 
