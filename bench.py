@@ -187,7 +187,8 @@ def lambda_path_bench(rank, world, epochs):
             res = [solve(lams[k]) for k in mine]
         e.record()
         torch.cuda.synchronize()
-        return s.elapsed_time(e), np.array([r["objective"] for r in res])
+        return (s.elapsed_time(e), np.array([r["objective"] for r in res]),
+                np.array([r["gap"] / abs(r["objective"]) for r in res]))
 
     conc = max(1, len(mine))
     solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=conc)
@@ -196,7 +197,7 @@ def lambda_path_bench(rank, world, epochs):
     else:
         solve(lams[mine[0]] if mine else lams[0])
     reps_c = [timed(solve) for _ in range(3)]
-    ms_c, obj_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
+    ms_c, obj_c, gap_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
     out.update(ms=ms_c, ms_reps=[r[0] for r in reps_c], concurrent=conc,
                bytes_per_update=solve.problem.bytes_per_update(), mean_blocks_per_row=solve.problem.mean_blocks_per_row())
     del solve
@@ -204,11 +205,13 @@ def lambda_path_bench(rank, world, epochs):
     serial = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=1)
     serial(lams[mine[0]] if mine else lams[0])  # warm-up
     reps_s = [timed(serial) for _ in range(3)]
-    ms_s, obj_s = sorted(reps_s, key=lambda r: r[0])[1]
+    ms_s, obj_s, gap_s = sorted(reps_s, key=lambda r: r[0])[1]
     del serial
     torch.cuda.empty_cache()
     out.update(ms_serial=ms_s, ms_serial_reps=[r[0] for r in reps_s],
-               max_rel_obj_diff=float(np.max(np.abs(obj_c - obj_s) / np.abs(obj_s))) if len(mine) else 0.0)
+               max_rel_obj_diff=float(np.max(np.abs(obj_c - obj_s) / np.abs(obj_s))) if len(mine) else 0.0,
+               certified_rel_gap=[float(f"{g:.3e}") for g in gap_c],
+               certified_rel_gap_serial=[float(f"{g:.3e}") for g in gap_s])
     return out
 
 
@@ -463,6 +466,8 @@ def main():
                  "rank0_serial_ms_reps": lp_local["ms_serial_reps"],
                  "serial_value": upd / (float(t[1].item()) / 1e3),
                  "max_rel_objective_diff_concurrent_vs_serial": float(t[2].item()),
+                 "rank0_certified_rel_gap_per_lambda": lp_local["certified_rel_gap"],
+                 "rank0_certified_rel_gap_per_lambda_serial": lp_local["certified_rel_gap_serial"],
                  "n_gpus": world, "algorithmic_bytes_per_update": lp_local["bytes_per_update"],
                  "mean_blocks_per_row": lp_local["mean_blocks_per_row"],
                  "roofline_frac_per_gpu": upd / (float(t[0].item()) / 1e3) / world * lp_local["bytes_per_update"]

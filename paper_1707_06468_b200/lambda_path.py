@@ -87,6 +87,17 @@ def run_path(lambdas, solve, rank=None, world=None):
     return sorted(allres, key=lambda r: r["index"])
 
 
+def _summary(dp, updates):
+    """Per-lambda result, reduced on the device: objective, Fenchel dual and
+    duality gap (a certificate: F(x) - F* <= gap), nnz and norm of x."""
+    parts = dp.objective_parts().cpu().numpy()
+    obj = float(parts.sum())
+    dual = float(dp.dual_objective_dev()[0].item())
+    xt = dp.field(0)
+    return {"objective": obj, "dual": dual, "gap": obj - dual, "nnz": int((xt != 0).sum().item()),
+            "norm": float(dp.torch.linalg.vector_norm(xt).item()), "updates": updates}
+
+
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
                   mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0, concurrent=1,
                   flags=0, hot=None):
@@ -118,12 +129,9 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
         else:
             dp.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas,
                          warps_per_cta=warps_per_cta, flags=flags, hot=hot)
-        parts = dp.objective_parts().cpu().numpy()
-        xt = dp.field(0)  # device vector; summaries reduced on the device
-        out = {"objective": float(parts.sum()), "nnz": int((xt != 0).sum().item()),
-               "norm": float(dp.torch.linalg.vector_norm(xt).item()), "updates": epochs * n}
+        out = _summary(dp, epochs * n)
         if keep_x:
-            out["x"] = xt.cpu().numpy()
+            out["x"] = dp.field(0).cpu().numpy()
         return out
 
     solve.problem = dp
@@ -155,12 +163,9 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
                                 warps_per_cta=warps_per_cta, flags=flags, hot=hot, stream=st)
                 torch.cuda.synchronize(dp.device)
                 for f, lam in zip(forks, wave):
-                    parts = f.objective_parts().cpu().numpy()
-                    xt = f.field(0)
-                    r = {"objective": float(parts.sum()), "nnz": int((xt != 0).sum().item()),
-                         "norm": float(torch.linalg.vector_norm(xt).item()), "updates": epochs * n}
+                    r = _summary(f, epochs * n)
                     if keep_x:
-                        r["x"] = xt.cpu().numpy()
+                        r["x"] = f.field(0).cpu().numpy()
                     out.append(r)
             return out
 
