@@ -149,7 +149,11 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
         forks = [dp] + [dp.fork() for _ in range(concurrent - 1)]
         streams = [torch.cuda.Stream(dp.device) for _ in range(concurrent)]
         sms = torch.cuda.get_device_properties(dp.device).multi_processor_count
-        ctas_each = ctas if ctas > 0 else max(1, sms // concurrent)
+        # 1/concurrent of the SMs each, but never more CTAs than the library's
+        # own grid for one solve (small problems cap the warps in flight at n/16)
+        own = dp.launch_config(dp._sched(n, ctas=0, warps_per_cta=warps_per_cta, flags=flags,
+                                         hot=bool(hot) if hot is not None else False))[0]
+        ctas_each = ctas if ctas > 0 else max(1, min(sms // concurrent, own))
 
         def batch(lams):
             out = []

@@ -84,11 +84,15 @@ def test_forks_are_independent_states(cuda, cfg5):
 
 def test_concurrent_path_matches_serial_objectives(cuda, cfg5):
     """The concurrent schedule (forks on streams, lane kernel) and the serial
-    one agree on every lambda's objective after the same epochs to 1e-5 (two
-    asynchronous runs of a not fully converged solve differ at ~1e-6)."""
+    one agree within their duality-gap certificates: both objectives are
+    >= F* and each is within its own gap of F*, so they differ by at most the
+    larger gap."""
     d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
     lams = lp.lambda_grid(pb.group_lambda_max(d, part), 6, 1e-1)
     serial = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="async"))
     conc = lp.run_path(lams, lp.device_solver(d, loss, part, epochs=200, mode="async", concurrent=6))
     for a, b in zip(serial, conc):
-        assert b["objective"] == pytest.approx(a["objective"], rel=1e-5), (a["lam"], a["objective"], b["objective"])
+        assert a["gap"] >= -1e-12 and b["gap"] >= -1e-12
+        tol = max(a["gap"], b["gap"]) + 1e-9 * abs(a["objective"])
+        assert abs(a["objective"] - b["objective"]) <= tol, (a["lam"], a["objective"], a["gap"], b["objective"],
+                                                             b["gap"])
