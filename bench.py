@@ -250,6 +250,44 @@ def big_config_bench(which, peak):
     return out
 
 
+def libsvm_bench(data):
+    """LibSVM ingestion, device parser vs the host routine
+    on config 2 written as LibSVM text with 6 significant digits (the device's
+    exact fast path); parsed datasets compared bitwise."""
+    import io
+
+    import paper_1707_06468_b200 as pb
+
+    f = data.features
+    text = "\n".join(f"{data.labels[i]:g} " + " ".join(f"{a + 1}:{b:.6g}" for a, b in zip(*f.row(i)))
+                     for i in range(f.n_rows)) + "\n"
+    pb.parse_libsvm(io.StringIO(text[:200000].rsplit("\n", 1)[0] + "\n"), device="auto")  # warm-up
+    raw = text.encode()
+    out = {"workload": "config 2 as LibSVM text (1e5 lines, 2e6 features, %.6g values), from bytes in memory",
+           "MB": len(raw) / 1e6}
+    res = {}
+    for tag, dev in (("device", "auto"), ("host", None)):
+        t0 = time.perf_counter()
+        res[tag] = _parse_bytes(pb, raw, dev)
+        out[f"{tag}_s"] = time.perf_counter() - t0
+        out[f"{tag}_MBps"] = out["MB"] / out[f"{tag}_s"]
+    a, b = res["device"].features, res["host"].features
+    out["identical"] = bool(np.array_equal(a.col_indices, b.col_indices) and np.array_equal(a.row_offsets, b.row_offsets)
+                            and np.array_equal(a.values.view(np.int64), b.values.view(np.int64))
+                            and np.array_equal(res["device"].labels, res["host"].labels))
+    return out
+
+
+def _parse_bytes(pb, raw, device):
+    import io
+
+    class _Raw(io.RawIOBase):  # a binary "file" whose read() returns the bytes, as open(path, "rb") does
+        def read(self, *a):
+            return raw
+
+    return pb.parse_libsvm(_Raw(), device=device)
+
+
 def _first_crossing(its, walls, rel, n, target):
     """Log-linear interpolation of the first crossing (asynchronous.py:213-230)
     on the RELATIVE gap; returns (seconds, epochs) or None."""
@@ -320,6 +358,7 @@ def main():
     ap.add_argument("--no-path", action="store_true")
     ap.add_argument("--no-big", action="store_true")
     ap.add_argument("--path-epochs", type=int, default=30)
+    ap.add_argument("--no-io", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -474,6 +513,9 @@ def main():
                  / 1e9 / peak}
 
     big = {}
+    ingest = None
+    if rank == 0 and world == 1 and not args.no_io:
+        ingest = libsvm_bench(data)
     if world == 1 and not args.no_big:
         for which in (3, 4):
             big[f"config{which}"] = big_config_bench(which, peak)
@@ -504,6 +546,7 @@ def main():
             "gpu_launches": 2 * args.steps,
             "cpu_baseline": cpu,
             "lambda_path": lpath,
+            "libsvm_ingest": ingest,
             "config3": big.get("config3"),
             "config4": big.get("config4"),
             "clocks": clocks,

@@ -218,6 +218,21 @@ int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params
 int ps_dual_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
                       int32_t x_stride, double *out, void *stream);
 
+/* LibSVM text -> CSR on the device (the reference's parse_libsvm,
+ * data.py:309-363).  `buf` holds the file's bytes on the device.
+ * ps_libsvm_index: start offset of each of the m lines (m = newlines + a final
+ * unterminated line).  ps_libsvm_scan: per line the label, feature count,
+ * status (0 ok, 1 blank/comment, 3 token without ':' at byte detail[j],
+ * 4 non-increasing index detail[j], 5 parse this line on the host: a number
+ * outside the exact fast path) and the largest index of the OK lines.
+ * ps_libsvm_fill: the OK lines' (idx - 1, value) pairs at
+ * row_ptr[row_of_line[j]]. */
+int ps_libsvm_index(const uint8_t *buf, int64_t n, int64_t *line_start, int64_t m, void *stream);
+int ps_libsvm_scan(const uint8_t *buf, int64_t n, const int64_t *line_start, int64_t m, double *labels,
+                   int32_t *nfeat, int32_t *status, int64_t *detail, unsigned long long *max_idx, void *stream);
+int ps_libsvm_fill(const uint8_t *buf, int64_t n, const int64_t *line_start, int64_t m, const int32_t *status,
+                   const int64_t *row_of_line, const int64_t *row_ptr, int64_t *cols, double *vals, void *stream);
+
 /* *dst = the device's %globaltimer (ns), stream-ordered (capturable into a
  * CUDA graph): checkpoint timing of DeviceProblem.run_async_checkpointed. */
 int ps_timestamp(unsigned long long *dst, void *stream);

@@ -33,7 +33,7 @@ EXPORTS = (
     "ps_coord_get_perm", "ps_coord_set_perm", "ps_atomic_gather",
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels", "ps_timestamp",
-    "ps_dual_objective", "ps_run_monitored",
+    "ps_dual_objective", "ps_run_monitored", "ps_libsvm_index", "ps_libsvm_scan", "ps_libsvm_fill",
 )
 
 _vp = ctypes.c_void_p
@@ -103,6 +103,9 @@ def load():
         "ps_state_reset": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
         "ps_timestamp": (_i32, [_vp, _vp]),
         "ps_dual_objective": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _i32, _vp, _vp]),
+        "ps_libsvm_index": (_i32, [_vp, _i64, _vp, _i64, _vp]),
+        "ps_libsvm_scan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+        "ps_libsvm_fill": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ps_run_monitored": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _vp, _P(Sched), _vp, _vp, _i64, _i32,
                                     _vp, _P(_i64), _P(ctypes.c_float), _P(_i32)]),
         "ps_hot_layout": (_i32, [_P(Csr), _vp, _vp, _i32, _i32, _f64, _P(_i32), _vp, _vp, _P(_i32), _P(_i64),

@@ -46,11 +46,6 @@ extern "C" int ps_device_count(void)
     return n;
 }
 
-#define CK(call, where)                                                    \
-    do {                                                                   \
-        cudaError_t _e = (call);                                           \
-        if (_e != cudaSuccess) return ps_cuda_fail(_e, where);             \
-    } while (0)
 
 // Scratch of the aux entry points comes from the device's default stream-
 // ordered pool.  Its release threshold defaults to 0, i.e. every synchronize
