@@ -218,6 +218,13 @@ int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params
 int ps_dual_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
                       int32_t x_stride, double *out, void *stream);
 
+/* FISTA (fista.py:38-58): x_new = prox_{h/L}(y - grad * inv_L) over all p
+ * coordinates (group penalty: per block of `part`), sums[0] = grad.(x_new - y),
+ * sums[1] = ||x_new - y||^2 (device); and y = x_new + beta (x_new - x). */
+int ps_fista_prox(const ps_part_t *part, const ps_params_t *prm, const double *y, const double *grad,
+                  double inv_L, int64_t p, double *x_new, double *sums, void *stream);
+int ps_fista_extrapolate(const double *x_new, const double *x, double beta, int64_t p, double *y, void *stream);
+
 /* LibSVM text -> CSR on the device (the reference's parse_libsvm,
  * data.py:309-363).  `buf` holds the file's bytes on the device.
  * ps_libsvm_index: start offset of each of the m lines (m = newlines + a final

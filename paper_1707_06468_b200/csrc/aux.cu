@@ -839,6 +839,115 @@ __global__ void __launch_bounds__(256) k_prox_group(const double *v, const doubl
     for (int64_t q = threadIdx.x; q < m; q += blockDim.x) out[q] = v[q] * f;
 }
 
+// ---------------------------------------------------------------------------
+// FISTA (fista.py:38-58): the prox-gradient trial point
+// x+ = prox_{h/L}(y - grad/L) over the whole vector (separable penalties per
+// coordinate, the group penalty per block of the partition) together with
+// grad.(x+ - y) and ||x+ - y||^2 for the backtracking test (per-CTA partials,
+// last CTA sums in a fixed order); and the extrapolation y' = x+ + beta (x+ - x).
+__global__ void __launch_bounds__(256) k_fista_prox(int kind, int G, int64_t nb, const int32_t *blk_ptr,
+                                                    const int32_t *blk_coords, int pen, double lam2, double lo,
+                                                    double hi, const double *y, const double *grad, double inv_L,
+                                                    int64_t p, double *xn, double *parts, unsigned *done,
+                                                    double *sums)
+{
+    double gd = 0.0, dd = 0.0;
+    if (pen != PS_PEN_GROUP) {
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+            const double u = y[j] - grad[j] * inv_L;
+            const double z = prox_sep(pen, u, inv_L, lam2, lo, hi);
+            const double df = z - y[j];
+            xn[j] = z;
+            gd += grad[j] * df;
+            dd += df * df;
+        }
+    } else {
+        for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+            int64_t q0, q1, g = 1;
+            if (kind == PS_PART_GENERAL) {
+                q0 = blk_ptr[b];
+                q1 = blk_ptr[b + 1];
+            } else {
+                g = kind == PS_PART_SINGLETON ? 1 : G;
+                q0 = b * g;
+                q1 = min((b + 1) * g, p);
+            }
+            double ss = 0.0;
+            for (int64_t q = q0; q < q1; q++) {
+                const int64_t j = kind == PS_PART_GENERAL ? blk_coords[q] : q;
+                const double u = y[j] - grad[j] * inv_L;
+                ss += u * u;
+            }
+            const double f = group_factor(sqrt(ss), inv_L, lam2);
+            for (int64_t q = q0; q < q1; q++) {
+                const int64_t j = kind == PS_PART_GENERAL ? blk_coords[q] : q;
+                const double z = (y[j] - grad[j] * inv_L) * f;
+                const double df = z - y[j];
+                xn[j] = z;
+                gd += grad[j] * df;
+                dd += df * df;
+            }
+        }
+    }
+    const int G1 = gridDim.x;
+    block_sum_store(gd, parts);
+    block_sum_store(dd, parts + G1);
+    __shared__ bool last;
+    __threadfence();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == (unsigned)gridDim.x - 1u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = 0; c < 2; c++) {
+        double v = 0.0;
+        for (int q = threadIdx.x; q < G1; q += blockDim.x) v += ld_cg(parts + (int64_t)c * G1 + q);
+        __shared__ double red[8];
+        v = warp_sum(v);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+            sums[c] = t;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fista_extrapolate(const double *xn, const double *x, double beta, int64_t p, double *y)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        y[j] = xn[j] + beta * (xn[j] - x[j]);
+}
+
+extern "C" int ps_fista_prox(const ps_part_t *part, const ps_params_t *prm, const double *y, const double *grad,
+                             double inv_L, int64_t p, double *x_new, double *sums, void *stream)
+{
+    if (!part || !prm || !y || !grad || !x_new || !sums || p < 1) return ps_fail(PS_EINVAL, "bad fista arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int G1 = std::max(1, sm_count() * 4);
+    double *parts = nullptr;
+    CK(pool_alloc((void **)&parts, sizeof(double) * (2 * G1 + 1), st), "ps_fista_prox alloc");
+    unsigned *done = reinterpret_cast<unsigned *>(parts + 2 * G1);
+    CK(cudaMemsetAsync(done, 0, sizeof(unsigned), st), "ps_fista_prox memset");
+    const int64_t nb = part->kind == PS_PART_SINGLETON ? p : part->n_blocks;
+    k_fista_prox<<<G1, 256, 0, st>>>(part->kind, part->G, nb, part->blk_ptr, part->blk_coords, prm->penalty,
+                                     prm->lam2, prm->lo, prm->hi, y, grad, inv_L, p, x_new, parts, done, sums);
+    CK(cudaGetLastError(), "ps_fista_prox launch");
+    CK(cudaFreeAsync(parts, st), "ps_fista_prox free");
+    return PS_OK;
+}
+
+extern "C" int ps_fista_extrapolate(const double *x_new, const double *x, double beta, int64_t p, double *y,
+                                    void *stream)
+{
+    if (!x_new || !x || !y || p < 1) return ps_fail(PS_EINVAL, "bad fista arguments");
+    k_fista_extrapolate<<<(int)std::min<int64_t>((p + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(x_new, x,
+                                                                                                          beta, p, y);
+    CK(cudaGetLastError(), "ps_fista_extrapolate launch");
+    return PS_OK;
+}
+
 extern "C" int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
                        void *stream)
 {
