@@ -8,12 +8,13 @@
 // whose numbers it can convert exactly:
 //   * indices: an optional sign and up to 18 decimal digits;
 //   * label / values: [sign] digits [. digits] [e|E [sign] digits] with at
-//     most 15 significant digits and a decimal exponent within +-22 -- then
-//     M * 10^E (or M / 10^-E) of two exact doubles is one correctly rounded
-//     operation (Clinger's fast path), i.e. exactly what float() returns.
-// A line with any other number (17-digit repr output, inf/nan, underscores,
-// huge exponents) is flagged "host" and the caller parses that line with the
-// reference semantics; definite errors (a token without ':', a
+//     most 19 significant digits, converted to the correctly rounded double
+//     (what float() returns): M * 10^E or M / 10^-E of two exact doubles when
+//     M < 2^53 and |E| <= 22 (Clinger), else Eisel-Lemire with the 128-bit
+//     powers of five of pow5_table.h (tools/gen_pow5.py).
+// A line with any other number (more digits, inf/nan, underscores, subnormal
+// or overflowing values) is flagged "host" and the caller parses that line
+// with the reference semantics; definite errors (a token without ':', a
 // non-increasing index) are reported with the byte offset / index so the
 // caller raises the same ParseError the reference would, at the first
 // offending line.
@@ -21,6 +22,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "pow5_table.h"
 
 using namespace ps;
 
@@ -36,7 +38,49 @@ __device__ __forceinline__ bool is_ws(uint8_t c)
 __constant__ double k_pow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                    1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
 
-// float() on [b, e) when the fast path applies; false -> the host decides
+// Eisel-Lemire (Lemire, "Number Parsing at a Gigabyte per Second", 2021;
+// the 128-bit power-of-five product suffices for <= 19 significant digits,
+// Mushtak & Lemire 2023): the correctly rounded double of w * 10^q, or false
+// for subnormal / overflowing results (left to the host).
+__device__ bool eisel_lemire(int64_t q, uint64_t w, double &out)
+{
+    if (w == 0 || q < POW5_MIN_Q) {
+        out = 0.0;
+        return true;
+    }
+    if (q > POW5_MAX_Q) return false;
+    const int lz = __clzll((long long)w);
+    w <<= lz;
+    const int idx = 2 * (int)(q - POW5_MIN_Q);
+    const uint64_t t_hi = __ldg(k_pow5_128 + idx), t_lo = __ldg(k_pow5_128 + idx + 1);
+    uint64_t hi = __umul64hi(w, t_hi), lo = w * t_hi;
+    if ((hi & 0x1FF) == 0x1FF) {
+        const uint64_t s_hi = __umul64hi(w, t_lo);
+        lo += s_hi;
+        if (s_hi > lo) hi++;
+    }
+    const int upper = (int)(hi >> 63);
+    const int shift = upper + 9;
+    uint64_t mant = hi >> shift;
+    int64_t p2 = (((152170 + 65536) * q) >> 16) + 63 + upper - lz + 1023;
+    if (p2 <= 0) return false;
+    if (lo <= 1 && q >= -4 && q <= 23 && (mant & 3) == 1 && (mant << shift) == hi) mant &= ~1ull;
+    mant += mant & 1;
+    mant >>= 1;
+    if (mant >= (2ull << 52)) {
+        mant = 1ull << 52;
+        p2++;
+    }
+    mant &= ~(1ull << 52);
+    if (p2 >= 2047) return false;
+    out = __longlong_as_double((long long)(((uint64_t)p2 << 52) | mant));
+    return true;
+}
+
+// float() on [b, e): decimal syntax with at most 19 significant digits,
+// converted exactly (Clinger's one-operation path when it applies, else
+// Eisel-Lemire); false -> the host decides (other syntax, more digits,
+// subnormal or overflowing values)
 __device__ bool parse_float_fast(const uint8_t *b, const uint8_t *e, double &out)
 {
     const uint8_t *p = b;
@@ -53,7 +97,7 @@ __device__ bool parse_float_fast(const uint8_t *b, const uint8_t *e, double &out
                 if (dot) frac++;  // leading zeros after the point shift the exponent only
                 continue;
             }
-            if (++sig > 15) return false;
+            if (++sig > 19) return false;
             m = m * 10 + (c - '0');
             if (dot) frac++;
         } else if (c == '.' && !dot) {
@@ -77,13 +121,14 @@ __device__ bool parse_float_fast(const uint8_t *b, const uint8_t *e, double &out
         if (eneg) ex = -ex;
     }
     if (p != e) return false;
+    const int E = ex - frac;
     double v;
     if (m == 0) {
         v = 0.0;
-    } else {
-        const int E = ex - frac;
-        if (E < -22 || E > 22) return false;
-        v = E >= 0 ? (double)m * k_pow10[E] : (double)m / k_pow10[-E];  // m < 10^15 < 2^53: exact operand
+    } else if (m < (1ull << 53) && E >= -22 && E <= 22) {
+        v = E >= 0 ? (double)m * k_pow10[E] : (double)m / k_pow10[-E];  // exact operands, one rounding
+    } else if (!eisel_lemire(E, m, v)) {
+        return false;
     }
     out = neg ? -v : v;
     return true;

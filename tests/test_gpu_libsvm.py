@@ -107,3 +107,41 @@ def test_large_generated_file_round_trip(cuda):
     dev, host = _both(text)
     _same(dev, host)
     assert dev.features.nnz == n * k
+
+
+def test_exact_conversion_of_17_digit_and_random_decimals(cuda):
+    """The device's Eisel-Lemire path: repr() of random doubles over the whole
+    normal range and random decimal strings of up to 19 digits parse to the
+    same bits as float() (the host routine); the device handles the file
+    (no host fallback decision)."""
+    import struct
+
+    from paper_1707_06468_b200 import data as D
+
+    rng = np.random.default_rng(17)
+    vals = []
+    bits = rng.integers(0, 2 ** 63, size=60_000, dtype=np.int64)
+    for b in bits:
+        x = struct.unpack("<d", struct.pack("<q", int(b)))[0]
+        if np.isfinite(x) and x != 0 and abs(x) > 2.3e-308:
+            vals.append(repr(float(x)))
+    for _ in range(60_000):
+        nd = int(rng.integers(1, 20))
+        s = "".join(str(int(c)) for c in rng.integers(0, 10, size=nd))
+        pos = int(rng.integers(0, nd + 1))
+        s = s[:pos] + "." + s[pos:]
+        if rng.random() < 0.5:
+            s += f"e{int(rng.integers(-290, 280))}"
+        if s[0] == "." and len(s) == 1:
+            continue
+        vals.append(s if rng.random() < 0.5 else "-" + s)
+    lines = []
+    for i in range(0, len(vals), 20):
+        chunk = vals[i:i + 20]
+        lines.append("1 " + " ".join(f"{j + 1}:{v}" for j, v in enumerate(chunk)))
+    text = "\n".join(lines) + "\n"
+    raw = text.encode()
+    dev = D._parse_device(raw, None)
+    assert dev is not None  # the device path handled it
+    host = pb.parse_libsvm(io.StringIO(text), device=None)
+    _same(dev, host)
