@@ -177,6 +177,14 @@ int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, v
 int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t m, double *out,
             void *stream);
 
+/* losses.py:73-86 loss derivative, elementwise: out[i] = l'(z[i], b[i]).
+ * fast = 0: the deterministic kernels' arithmetic (libdevice exp, IEEE
+ * division: bit-identical to the reference's scalar formula); fast = 1: the
+ * asynchronous kernels' (exp_nonpos + reciprocal-Newton division, ~1 ulp).
+ * Device pointers; an inspection / test hook for the kernels' loss code. */
+int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
+                  void *stream);
+
 /* Hot layout (SINGLETON: unit = 1, columns; CONTIG: unit = G, whole blocks):
  * units present in at least max(ceil(min_frac * n), theta) rows — theta the
  * smallest threshold letting at most hot_max units qualify — are the H hot

@@ -98,7 +98,8 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
             # the reference's live monitor: one launch, inconsistent snapshots of
             # the running solve at the checkpoint marks (ps_run_monitored)
             its, objs, secs = dp.run_async_monitored(total, every, gamma, seed=config.seed, ctas=ctas,
-                                                     warps_per_cta=wpc, contention=config.contention)
+                                                     warps_per_cta=wpc, contention=config.contention,
+                                                     skip_first=True)
             its, objs, secs = its[1:], objs[1:], secs[1:]  # checkpoint 0 is recorded above
         else:  # snapshots too large for host memory: stop at each mark (device-pipelined objectives)
             its, objs, secs = dp.run_async_checkpointed(total, every, gamma, seed=config.seed, ctas=ctas,

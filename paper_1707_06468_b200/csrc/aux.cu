@@ -123,28 +123,60 @@ __global__ void k_finish_sum(const double *parts, int nparts, int ncols, double 
 // ---------------------------------------------------------------------------
 // ps_prepare kernels
 
-// per row: ||a_i||^2 (losses.py:99-105 via data.py:74-80), nnz; atomic maxima.
+// per row: ||a_i||^2 (losses.py:99-105 via data.py:74-80), nnz; maxima
+// reduced per warp first (one atomic per warp, not per row: a per-row atomic
+// on one address serialises ~n L2 operations).
 template <typename VT, typename PT>
 __global__ void k_rowstats(const void *row_ptr, const void *val, int64_t n, unsigned long long *max_sq,
                            int *max_nnz)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
     double s = 0.0;
-    for (int64_t e = lo; e < hi; e++) {
-        double v = rvx<VT>(val, e);
-        s += v * v;
+    int k = 0;
+    if (i < n) {
+        int64_t lo = rpx<PT>(row_ptr, i), hi = rpx<PT>(row_ptr, i + 1);
+        for (int64_t e = lo; e < hi; e++) {
+            double v = rvx<VT>(val, e);
+            s += v * v;
+        }
+        k = (int)(hi - lo);
     }
-    atomicMax(max_sq, (unsigned long long)__double_as_longlong(s));  // s >= 0: bit order == value order
-    atomicMax(max_nnz, (int)(hi - lo));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    k = __reduce_max_sync(0xffffffffu, k);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(max_sq, (unsigned long long)__double_as_longlong(s));  // s >= 0: bit order == value order
+        atomicMax(max_nnz, k);
+    }
 }
 
 // singleton: n_j = #rows containing column j (columns distinct within a row).
-__global__ void k_count_cols(const int32_t *col, int64_t nnz, int32_t *counts)
+// The leading CNT_HEAD columns are counted per CTA in shared memory first: a
+// Zipf head column sits in almost every row, and a global atomic per nonzero
+// queues ~n operations on its L2 line (config 2: 0.25 ms -> ~10 us).  Hot
+// columns are in the head both in original order (Zipf rank = index) and
+// after ps_hot_layout (hot rank r at index r * stride).
+constexpr int CNT_HEAD = 8192;
+__global__ void __launch_bounds__(512) k_count_cols(const int32_t *col, int64_t nnz, int64_t p, int32_t *counts)
 {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(counts + col[e], 1);
+    __shared__ int32_t bins[CNT_HEAD];
+    const int hb = p < (int64_t)CNT_HEAD ? (int)p : CNT_HEAD;
+    for (int j = threadIdx.x; j < hb; j += blockDim.x) bins[j] = 0;
+    __syncthreads();
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = col[e];
+        if (c < hb) atomicAdd(bins + c, 1);
+        else atomicAdd(counts + c, 1);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < hb; j += blockDim.x)
+        if (bins[j]) atomicAdd(counts + j, bins[j]);
+}
+static void count_cols(const int32_t *col, int64_t nnz, int64_t p, int32_t *counts, int sms, cudaStream_t st)
+{
+    // enough nonzeros per CTA that the head flush (CNT_HEAD bins) stays small
+    int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 4, (nnz + 4095) / 4096));
+    k_count_cols<<<(int)ctas, 512, 0, st>>>(col, nnz, p, counts);
 }
 
 // contiguous groups: count each distinct block of a row once; max slots.
@@ -212,15 +244,27 @@ __global__ void k_index_general(const void *row_ptr, const int32_t *col, int64_t
     }
 }
 
-// data.py:259-262: d_B = n / n_B (0 for dead), max n_B, dead count.
+// data.py:259-262: d_B = n / n_B (0 for dead), max n_B, dead count (warp
+// reductions, one atomic per warp).
 __global__ void k_weights(const int32_t *counts, int64_t nb, int64_t n, double *w, unsigned long long *maxc,
                           unsigned long long *dead)
 {
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-        int c = counts[b];
-        w[b] = c > 0 ? (double)n / (double)c : 0.0;
-        if (c == 0) atomicAdd(dead, 1ull);
-        atomicMax(maxc, (unsigned long long)c);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t end = (nb + 31) / 32 * 32;  // whole warps stay in the loop
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < end; b += stride) {
+        int c = 0;
+        unsigned nd = 0;
+        if (b < nb) {
+            c = counts[b];
+            w[b] = c > 0 ? (double)n / (double)c : 0.0;
+            nd = c == 0;
+        }
+        c = __reduce_max_sync(0xffffffffu, c);
+        nd = __reduce_add_sync(0xffffffffu, nd);
+        if ((threadIdx.x & 31) == 0) {
+            if (nd) atomicAdd(dead, (unsigned long long)nd);
+            atomicMax(maxc, (unsigned long long)c);
+        }
     }
 }
 
@@ -265,7 +309,7 @@ extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, p
 
     int grid = sm_count() * 8;
     if (part->kind == PS_PART_SINGLETON) {
-        if (csr->nnz > 0) k_count_cols<<<grid, tb, 0, st>>>(csr->col_idx, csr->nnz, part->blk_count);
+        if (csr->nnz > 0) count_cols(csr->col_idx, csr->nnz, p, part->blk_count, sm_count(), st);
     } else if (part->kind == PS_PART_CONTIG) {
         if (i64) k_count_contig<long long><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->G, part->blk_count, max_slots);
         else k_count_contig<int><<<rows_grid, tb, 0, st>>>(csr->row_ptr, csr->col_idx, n, part->G, part->blk_count, max_slots);
@@ -1243,7 +1287,7 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
     int rows_grid = (int)((n + 255) / 256);
     CK(cudaMemsetAsync(counts_ws, 0, sizeof(int32_t) * nu, st), "ps_hot_layout memset");
     if (nnz > 0) {
-        if (unit == 1) k_count_cols<<<grid, 256, 0, st>>>(col_inout, nnz, counts_ws);
+        if (unit == 1) count_cols(col_inout, nnz, p, counts_ws, sm_count(), st);
         else if (i64) k_count_units<long long><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
         else k_count_units<int><<<rows_grid, 256, 0, st>>>(csr->row_ptr, col_inout, n, unit, counts_ws);
     }

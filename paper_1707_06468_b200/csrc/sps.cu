@@ -727,14 +727,63 @@ __device__ __forceinline__ double prox_t(double u, double eff, double lam2, int 
     return prox_sep(pen, u, eff, lam2, lo, hi);
 }
 
+// exp(x) for x <= 0 (or NaN), ~1 ulp: x = n ln2 + r (Cody-Waite, |r| <= ln2/2),
+// exp(r) by its degree-12 Taylor polynomial (truncation < 2e-16 relative),
+// 2^n applied as two exact power-of-two factors so subnormal results round
+// once.  About 20 instructions against ~49 for the libdevice exp(), whose
+// range checks this domain does not need.  Used by the asynchronous kernels
+// only (async parity is on the objective); the deterministic replay keeps
+// the libdevice exp of loss_deriv.
+__device__ __forceinline__ double exp_nonpos(double x)
+{
+    x = x < -746.0 ? -746.0 : x;  // exp(-746) rounds to 0; keeps n in int range (NaN passes)
+    const double shifter = 0x1.8p52;
+    double kd = __fma_rn(x, 0x1.71547652b82fep+0, shifter);  // n = rint(x / ln2) in the low bits
+    const int n = __double2loint(kd);
+    kd = __dsub_rn(kd, shifter);
+    double r = __fma_rn(kd, -0x1.62e4200000000p-1, x);  // ln2_hi: kd * ln2_hi is exact
+    r = __fma_rn(kd, -0x1.fdf473de6af28p-22, r);
+    double q = 0x1.1eed8eff8d898p-29;  // 1/12!
+    q = __fma_rn(q, r, 0x1.ae64567f544e4p-26);
+    q = __fma_rn(q, r, 0x1.27e4fb7789f5cp-22);
+    q = __fma_rn(q, r, 0x1.71de3a556c734p-19);
+    q = __fma_rn(q, r, 0x1.a01a01a01a01ap-16);
+    q = __fma_rn(q, r, 0x1.a01a01a01a01ap-13);
+    q = __fma_rn(q, r, 0x1.6c16c16c16c17p-10);
+    q = __fma_rn(q, r, 0x1.1111111111111p-7);
+    q = __fma_rn(q, r, 0x1.5555555555555p-5);
+    q = __fma_rn(q, r, 0x1.5555555555555p-3);
+    q = __fma_rn(q, r, 0.5);
+    q = __fma_rn(q, r, 1.0);
+    q = __fma_rn(q, r, 1.0);
+    const int n1 = n >> 1, n2 = n - n1;  // n in [-1076, 0]: both halves >= -538
+    q = __dmul_rn(q, __hiloint2double((n1 + 1023) << 20, 0));
+    return __dmul_rn(q, __hiloint2double((n2 + 1023) << 20, 0));
+}
+
+// num / den for den in [1, 2] (den = 1 + exp(-|t|)): hardware reciprocal
+// estimate, two Newton steps and one residual correction (faithful, no
+// special cases in this domain).
+__device__ __forceinline__ double div_1to2(double num, double den)
+{
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(den));
+    double e = __fma_rn(-den, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-den, y, 1.0);
+    y = __fma_rn(y, e, y);
+    const double q = __dmul_rn(num, y);
+    return __fma_rn(__fma_rn(-den, q, num), y, q);
+}
+
 // losses.py:73-86 with one division: et = exp(-|t|); sig = (t > 0 ? 1 : et) / (1 + et)
 // -- the same two expressions as the reference's branches, no divergence.
 template <int LOSS> __device__ __forceinline__ double deriv_t(double z, double b)
 {
     if (LOSS == PS_LOSS_LOGISTIC) {
         double t = -b * z;
-        double et = exp(-fabs(t));
-        double sig = (t > 0 ? 1.0 : et) / (1.0 + et);
+        double et = exp_nonpos(-fabs(t));
+        double sig = div_1to2(t > 0 ? 1.0 : et, 1.0 + et);
         return -b * sig;
     }
     return z - b;
@@ -1835,5 +1884,31 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     for (int k = 0; k < ns; k++) MCK(cudaEventElapsedTime(snap_ms + k, ev0, evs[k]), "monitor timing");
     *n_snaps = ns;
 #undef MCK
+    return PS_OK;
+}
+
+// ps_loss_deriv: the kernels' loss derivative applied elementwise (test /
+// inspection hook).  fast = 1 is the asynchronous kernels' deriv_t.
+namespace ps {
+__global__ void k_loss_deriv(int loss, int fast, const double *z, const double *b, int64_t m, double *out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!fast) out[i] = loss_deriv(loss, z[i], b[i]);
+        else out[i] = loss == PS_LOSS_LOGISTIC ? deriv_t<PS_LOSS_LOGISTIC>(z[i], b[i])
+                                               : deriv_t<PS_LOSS_SQUARED>(z[i], b[i]);
+    }
+}
+}  // namespace ps
+
+extern "C" int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
+                             void *stream)
+{
+    if (loss != PS_LOSS_LOGISTIC && loss != PS_LOSS_SQUARED) return ps_fail(PS_EINVAL, "unknown loss");
+    if (m < 0 || (m > 0 && (!z || !b || !out))) return ps_fail(PS_EINVAL, "bad loss_deriv arguments");
+    if (m == 0) return PS_OK;
+    ps::k_loss_deriv<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(loss, fast, z,
+                                                                                                       b, m, out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return ps_cuda_fail(e, "ps_loss_deriv launch");
     return PS_OK;
 }

@@ -298,7 +298,7 @@ class DeviceProblem:
         self.slot_base += int(count)
 
     def run_async_monitored(self, total, every, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=4.0,
-                            hot=None, hot_period=0, flags=0, gap=False):
+                            hot=None, hot_period=0, flags=0, gap=False, skip_first=False):
         """`total` lock-free updates in ONE launch with the reference's live
         monitor (asynchronous.py:181-198, ps_run_monitored): each time the
         progress counter crosses a multiple of `every`, the live coordinate
@@ -306,7 +306,10 @@ class DeviceProblem:
         the warps keep going.  The objectives (and with ``gap`` the Fenchel
         duals) of the snapshots are evaluated afterwards; a checkpoint's time is
         its snapshot's device time plus one measured objective evaluation (the
-        time the monitor would need to know it).  Returns (iterations,
+        time the monitor would need to know it).  The last snapshot is the
+        consistent state after the launch and is evaluated in place;
+        ``skip_first`` leaves checkpoint 0 (the starting state, which the caller
+        already knows) unevaluated (objective 0.0).  Returns (iterations,
         objectives, seconds[, duals])."""
         torch = self.torch
         if hot is None:
@@ -328,17 +331,25 @@ class DeviceProblem:
         outs = torch.zeros((k, 4), dtype=torch.float64, device=self.device)
         duals = torch.zeros((k, 2), dtype=torch.float64, device=self.device) if gap else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        buf = torch.empty((self.p_dev, 4), dtype=torch.float64, device=self.device)
+        buf = None
         for j in range(k):
-            buf.copy_(snaps[j])
+            if j == 0 and skip_first:
+                continue
+            if j == k - 1:
+                src = self.coord  # the final snapshot is the (consistent) state after the launch
+            else:
+                if buf is None:
+                    buf = torch.empty((self.p_dev, 4), dtype=torch.float64, device=self.device)
+                buf.copy_(snaps[j])
+                src = buf
             if j == 1:
                 e0.record()
-            _lib.check(L.ps_objective(self.csr, self.part, self.params(), buf.data_ptr(), 4,
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), src.data_ptr(), 4,
                                       outs[j].data_ptr(), _lib.stream_ptr()))
             if j == 1:
                 e1.record()
             if gap:
-                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), buf.data_ptr(), 4,
+                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), src.data_ptr(), 4,
                                                duals[j].data_ptr(), _lib.stream_ptr()))
         torch.cuda.synchronize(self.device)
         t_eval = e0.elapsed_time(e1) / 1e3 if k > 1 else 0.0

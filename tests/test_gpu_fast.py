@@ -199,3 +199,50 @@ def test_run_async_api_uses_the_live_monitor(cuda):
     assert tr.iterations[0] == 0 and tr.iterations[-1] == 20 * data.n_samples
     assert all(b >= a for a, b in zip(tr.iterations, tr.iterations[1:]))
     assert len(tr.objective) >= 3 and tr.objective[-1] < tr.objective[0]
+
+
+def _ulps(a, b):
+    ia, ib = a.view(np.int64), b.view(np.int64)
+    return np.abs(ia - ib)
+
+
+def test_async_loss_derivative_accuracy(cuda):
+    """The asynchronous kernels' logistic derivative (exp_nonpos + reciprocal
+    Newton division, ps_loss_deriv fast=1) against the deterministic kernels'
+    (libdevice exp + IEEE division, the reference's formula losses.py:73-86):
+    within 2 ulp everywhere (subnormal results included), the same NaNs, over
+    margins spanning the underflow range of exp."""
+    import torch
+
+    from paper_1707_06468_b200 import _lib
+
+    rng = np.random.default_rng(0)
+    z = np.concatenate([rng.uniform(-40, 40, 200000), rng.uniform(-800, 800, 200000),
+                        rng.standard_normal(100000) * 1e-3,
+                        [0.0, -0.0, 1e-300, -1e-300, 700.0, -700.0, 708.5, 744.9, 745.2, 746.0, -746.0, 1e6, -1e6,
+                         np.inf, -np.inf, np.nan]])
+    b = np.where(rng.random(z.size) < 0.5, -1.0, 1.0)
+    zd, bd = torch.from_numpy(z).cuda(), torch.from_numpy(b).cuda()
+    outs = []
+    for fast in (0, 1):
+        o = torch.empty_like(zd)
+        _lib.check(_lib.load().ps_loss_deriv(0, fast, zd.data_ptr(), bd.data_ptr(), z.size, o.data_ptr(), 0))
+        outs.append(o.cpu().numpy())
+    ref, fast = outs
+    assert np.array_equal(np.isnan(ref), np.isnan(fast))
+    ok = ~np.isnan(ref)
+    # ulps of the int64 views: same-sign values, so zeros and subnormals are
+    # measured on the same scale (exp underflow rounds within one subnormal ulp)
+    assert np.array_equal(np.signbit(ref[ok]), np.signbit(fast[ok]))
+    assert _ulps(ref[ok], fast[ok]).max() <= 2
+    # the deterministic path restates losses.py:73-86 (numpy, same branches)
+    t = -b * z
+    with np.errstate(over="ignore", invalid="ignore"):
+        sig = np.where(t > 0, 1.0 / (1.0 + np.exp(-np.abs(t))), np.exp(-np.abs(t)) / (1.0 + np.exp(-np.abs(t))))
+    npref = -b * sig
+    assert np.allclose(ref[ok], npref[ok], rtol=1e-15, atol=0)
+    # squared loss: z - b in both
+    o = torch.empty_like(zd)
+    _lib.check(_lib.load().ps_loss_deriv(1, 1, zd.data_ptr(), bd.data_ptr(), z.size, o.data_ptr(), 0))
+    sq = o.cpu().numpy()
+    assert np.array_equal(sq[ok], (z - b)[ok])
