@@ -91,24 +91,27 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
         dist = float(np.sum((dp.x() - track_distance_to) ** 2)) if track else None
         trace.append(it, n, obj, time.perf_counter() - start, distance=dist, threads=config.threads)
 
-    checkpoint(0)
-    if not single and not track:
-        nseg = -(-total // every)
-        if dp.p_dev * 32 * (nseg + 2) <= (4 << 30):
-            # the reference's live monitor: one launch, inconsistent snapshots of
-            # the running solve at the checkpoint marks (ps_run_monitored)
-            its, objs, secs = dp.run_async_monitored(total, every, gamma, seed=config.seed, ctas=ctas,
-                                                     warps_per_cta=wpc, contention=config.contention,
-                                                     skip_first=True)
-            its, objs, secs = its[1:], objs[1:], secs[1:]  # checkpoint 0 is recorded above
-        else:  # snapshots too large for host memory: stop at each mark (device-pipelined objectives)
-            its, objs, secs = dp.run_async_checkpointed(total, every, gamma, seed=config.seed, ctas=ctas,
-                                                        warps_per_cta=wpc, contention=config.contention)
+    nseg = -(-total // every)
+    if not single and not track and dp.p_dev * 32 * (nseg + 2) <= (4 << 30):
+        # the reference's live monitor: one launch, inconsistent snapshots of the
+        # running solve at the checkpoint marks (ps_run_monitored); checkpoint 0
+        # is evaluated on the device ahead of the launch
+        its, objs, secs = dp.run_async_monitored(total, every, gamma, seed=config.seed, ctas=ctas,
+                                                 warps_per_cta=wpc, contention=config.contention)
+        for it, ob, sc in zip(its, objs, secs):
+            trace.append(it, n, ob, sc, threads=config.threads)
+        done = total
+    elif not single and not track:
+        # snapshots too large for host memory: stop at each mark (device-pipelined objectives)
+        checkpoint(0)
+        its, objs, secs = dp.run_async_checkpointed(total, every, gamma, seed=config.seed, ctas=ctas,
+                                                    warps_per_cta=wpc, contention=config.contention)
         t0 = trace.wall_seconds[0]
         for it, ob, sc in zip(its, objs, secs):
             trace.append(it, n, ob, t0 + sc, threads=config.threads)
         done = total
     else:
+        checkpoint(0)
         done = 0
     while done < total:
         nxt = min(total, done + every)

@@ -95,8 +95,16 @@ class DeviceProblem:
                 self.col = up(f.col_indices).to(torch.int32)
                 val_d, y_d = up(f.values), up(np.asarray(labels))
                 if value_dtype == "auto":
-                    use32 = all(t.dtype == torch.float32 or bool(torch.equal(t.to(torch.float32).to(t.dtype), t))
-                                for t in (val_d, y_d))
+                    # fp32 storage when lossless: small arrays are checked on the host
+                    # (no device round trip), large fp64 ones on the device
+                    def exact32(host, t):
+                        if t.dtype == torch.float32:
+                            return True
+                        if t.numel() <= (1 << 20):
+                            return _f32_exact(host)
+                        return bool(torch.equal(t.to(torch.float32).to(t.dtype), t))
+
+                    use32 = exact32(f.values, val_d) and exact32(labels, y_d)
                 else:
                     use32 = np.dtype(value_dtype) == np.float32
                 self.value_type = _lib.F32 if use32 else _lib.F64
@@ -107,7 +115,7 @@ class DeviceProblem:
                                 self.val.data_ptr(), self.y.data_ptr(), self.row_ptr_type, self.value_type)
             # ---- partition (+ hot-column renumbering for singleton layouts)
             self._setup_partition(partition)
-            self.H, self.hot_shift, self.perm, self.perm_np, self.p_dev = 0, 0, None, None, self.p
+            self.H, self.hot_shift, self.perm, self._perm_np, self.p_dev = 0, 0, None, None, self.p
             self.hot_unit = 1 if self.part_kind == "singleton" else int(self.part.G)
             if hot_max is None:
                 # staged columns: 512, or 1024 when the coordinate records (32 B each)
@@ -120,9 +128,11 @@ class DeviceProblem:
                 units = hot_max if self.hot_unit == 1 else max(1, min(4 * hot_max, 1024) // self.hot_unit)
                 self._hot_layout(int(units), float(hot_min_frac), int(hot_stride))
             # ---- state
-            self.coord = torch.zeros((self.p_dev, 4), dtype=torch.float64, device=dev)
-            self.alpha = torch.zeros(self.n, dtype=torch.float64, device=dev)
-            self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+            # one zeroed allocation (one fill) for coord[p, 4], alpha[n] and the counter
+            state = torch.zeros(4 * self.p_dev + self.n + 1, dtype=torch.float64, device=dev)
+            self.coord = state[:4 * self.p_dev].view(self.p_dev, 4)
+            self.alpha = state[4 * self.p_dev:4 * self.p_dev + self.n]
+            self.counter = state[-1:].view(torch.int64)
             self.stats = _lib.Stats()
             _lib.check(_lib.load().ps_prepare(self.csr, self.part, self.coord.data_ptr(), self.stats,
                                               _lib.stream_ptr()))
@@ -211,8 +221,20 @@ class DeviceProblem:
         self.hot_shift = S.value.bit_length() - 1
         self.p_dev = int(pp.value)
         self.csr.n_cols = self.p_dev
-        self.perm_np = self.perm.cpu().numpy().astype(np.int64)
-        self.unit_perm_np = self.perm_np[::G] // G if G > 1 else self.perm_np
+        self._perm_np = None  # host copy made on first use (perm_np)
+
+    @property
+    def perm_np(self):
+        """original -> stored coordinate index (host int64), or None without a hot layout"""
+        if self.perm is not None and self._perm_np is None:
+            self._perm_np = self.perm.cpu().numpy().astype(np.int64)
+        return self._perm_np
+
+    @property
+    def unit_perm_np(self):
+        G = self.hot_unit
+        pn = self.perm_np
+        return pn[::G] // G if (pn is not None and G > 1) else pn
 
     def _to_stored(self, v):
         """original-order vector -> stored (permuted, padded) order"""
@@ -298,7 +320,7 @@ class DeviceProblem:
         self.slot_base += int(count)
 
     def run_async_monitored(self, total, every, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=4.0,
-                            hot=None, hot_period=0, flags=0, gap=False, skip_first=False):
+                            hot=None, hot_period=0, flags=0, gap=False):
         """`total` lock-free updates in ONE launch with the reference's live
         monitor (asynchronous.py:181-198, ps_run_monitored): each time the
         progress counter crosses a multiple of `every`, the live coordinate
@@ -306,10 +328,9 @@ class DeviceProblem:
         the warps keep going.  The objectives (and with ``gap`` the Fenchel
         duals) of the snapshots are evaluated afterwards; a checkpoint's time is
         its snapshot's device time plus one measured objective evaluation (the
-        time the monitor would need to know it).  The last snapshot is the
-        consistent state after the launch and is evaluated in place;
-        ``skip_first`` leaves checkpoint 0 (the starting state, which the caller
-        already knows) unevaluated (objective 0.0).  Returns (iterations,
+        time the monitor would need to know it).  Checkpoint 0 (the starting
+        state) and the last one (the consistent state after the launch) are
+        evaluated in place, without a copy.  Returns (iterations,
         objectives, seconds[, duals])."""
         torch = self.torch
         if hot is None:
@@ -323,41 +344,50 @@ class DeviceProblem:
         ms = (ctypes.c_float * nmax)()
         ns = ctypes.c_int32(0)
         L = _lib.load()
+        outs = torch.zeros((nmax, 4), dtype=torch.float64, device=self.device)
+        duals = torch.zeros((nmax, 2), dtype=torch.float64, device=self.device) if gap else None
+
+        def evaluate(j, ptr):
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), ptr, 4, outs[j].data_ptr(),
+                                      _lib.stream_ptr()))
+            if gap:
+                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), ptr, 4, duals[j].data_ptr(),
+                                               _lib.stream_ptr()))
+
+        # checkpoint 0 is the state the launch starts from: evaluated in place,
+        # stream-ordered before it (no copy, no host round trip)
+        evaluate(0, self.coord.data_ptr())
         _lib.check(L.ps_run_monitored(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(), int(every), nmax,
                                       snaps.data_ptr(), counts, ms, ctypes.byref(ns)))
         self.slot_base += int(total)
         k = ns.value
-        outs = torch.zeros((k, 4), dtype=torch.float64, device=self.device)
-        duals = torch.zeros((k, 2), dtype=torch.float64, device=self.device) if gap else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         buf = None
-        for j in range(k):
-            if j == 0 and skip_first:
-                continue
+        for j in range(1, k):
             if j == k - 1:
-                src = self.coord  # the final snapshot is the (consistent) state after the launch
+                ptr = self.coord.data_ptr()  # the final snapshot is the (consistent) state after the launch
             else:
                 if buf is None:
                     buf = torch.empty((self.p_dev, 4), dtype=torch.float64, device=self.device)
                 buf.copy_(snaps[j])
-                src = buf
+                ptr = buf.data_ptr()
             if j == 1:
                 e0.record()
-            _lib.check(L.ps_objective(self.csr, self.part, self.params(), src.data_ptr(), 4,
-                                      outs[j].data_ptr(), _lib.stream_ptr()))
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), ptr, 4, outs[j].data_ptr(),
+                                      _lib.stream_ptr()))
             if j == 1:
                 e1.record()
             if gap:
-                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), src.data_ptr(), 4,
-                                               duals[j].data_ptr(), _lib.stream_ptr()))
-        torch.cuda.synchronize(self.device)
+                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), ptr, 4, duals[j].data_ptr(),
+                                               _lib.stream_ptr()))
+        o = outs[:k].cpu().numpy()  # synchronizes
         t_eval = e0.elapsed_time(e1) / 1e3 if k > 1 else 0.0
-        objs = outs[:, :3].sum(dim=1).cpu().numpy().tolist()
+        objs = [float(v[0] + v[1] + v[2]) for v in o]  # the order objective() sums in
         its = [int(counts[j]) for j in range(k)]
         secs = [float(ms[j]) / 1e3 + (t_eval if j > 0 else 0.0) for j in range(k)]
         if gap:
-            return its, objs, secs, duals[:, 0].cpu().numpy().tolist()
+            return its, objs, secs, duals[:k, 0].cpu().numpy().tolist()
         return its, objs, secs
 
     def run_async_checkpointed(self, total, every, gamma, seed=0, ring=4, graph=False, gap=False, **kw):

@@ -240,7 +240,9 @@ def test_async_loss_derivative_accuracy(cuda):
     with np.errstate(over="ignore", invalid="ignore"):
         sig = np.where(t > 0, 1.0 / (1.0 + np.exp(-np.abs(t))), np.exp(-np.abs(t)) / (1.0 + np.exp(-np.abs(t))))
     npref = -b * sig
-    assert np.allclose(ref[ok], npref[ok], rtol=1e-15, atol=0)
+    nrm = ok & (np.abs(npref) >= np.finfo(np.float64).tiny)  # subnormals: libm and libdevice round differently
+    u = _ulps(ref[nrm], npref[nrm])
+    assert u.max() <= 2, (u.max(), z[nrm][np.argmax(u)])
     # squared loss: z - b in both
     o = torch.empty_like(zd)
     _lib.check(_lib.load().ps_loss_deriv(1, 1, zd.data_ptr(), bd.data_ptr(), z.size, o.data_ptr(), 0))
