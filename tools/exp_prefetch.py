@@ -1,5 +1,7 @@
 """A/B of the fast kernel's CSR L2 prefetch distance on the large configs
-(ps_sched_t.flags bits 16..19: 15 = off, d = distance).
+(ps_sched_t.flags bits 16..19: 15 = off, d = distance).  The prefetch was
+measured (config 3 -3%, config 4 +-0) and removed from
+the kernel, so on the current library every variant runs the same code.
     python tools/exp_prefetch.py 3 [dists...]"""
 import json, sys
 from pathlib import Path
