@@ -123,6 +123,8 @@ typedef struct ps_sched {
                                      reference's literal scatter_add (asynchronous.py:105-107);
                                      default: store 0 */
 /* bits 8..15: extra divisor of the staged columns' contention scale */
+#define PS_FLAG_MON_ENDS_IN_PLACE 65536 /* ps_run_monitored: skip the copies of the first and last
+                                           snapshots (the caller reads coord itself) */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);
@@ -214,7 +216,10 @@ int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned 
  * snaps[k] (pinned HOST memory: a copy-engine DMA beside the kernel).  snaps[0] is the state before the first update,
  * the last one the state after the launch; snap_counts / snap_ms (host) get
  * the counter value and the device time (ms since the launch) of each;
- * *n_snaps <= max_snaps.  The solve never stops for a checkpoint. */
+ * *n_snaps <= max_snaps.  The solve never stops for a checkpoint.  With
+ * PS_FLAG_MON_ENDS_IN_PLACE in sched->flags, snaps[0] and the last snapshot
+ * are not copied (their counts and times are still reported): the caller
+ * evaluates those two states on coord itself, before and after the call. */
 int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
                      double *alpha, const ps_sched_t *sched, void *scratch, void *stream, int64_t every,
                      int32_t max_snaps, double *snaps, int64_t *snap_counts, float *snap_ms, int32_t *n_snaps);

@@ -1320,7 +1320,7 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
     CK(cudaFreeAsync(cand, st), "ps_hot_layout free");
     int S = *stride_inout;
     while (S > 1 && (int64_t)S * H > nu) S >>= 1;  // hot units at 0, S, 2S, ... (unit indices)
-    const int64_t chunk = 1 << 12;
+    const int64_t chunk = 1 << 10;  // one warp per chunk in k_perm: enough chunks to fill the GPU
     int nb = (int)((nu + chunk - 1) / chunk);
     int64_t *sums = nullptr;
     int32_t *perm_u = nullptr, *inv_u = nullptr;
@@ -1342,7 +1342,8 @@ extern "C" int ps_hot_layout(const ps_csr_t *csr, int32_t *col_inout, void *val_
     CK(cudaFreeAsync(perm_u, st), "ps_hot_layout free");
     CK(cudaFreeAsync(sums, st), "ps_hot_layout free");
     CK(cudaFreeAsync(cnt, st), "ps_hot_layout free");
-    CK(cudaStreamSynchronize(st), "ps_hot_layout sync");
+    // no final synchronize: the permutation, remap and row sort are stream-ordered
+    // before any later use of col / val / perm on this stream
     *H_out = H;
     *stride_inout = S;
     *p_pad_out = nu * unit;

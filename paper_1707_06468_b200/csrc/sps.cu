@@ -1844,15 +1844,20 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     unsigned long long *h_cnt = m.h_cnt;
     MCK(cudaMemsetAsync(sched->counter, 0, sizeof(unsigned long long), st), "monitor counter reset");
     MCK(cudaEventRecord(ev0, st), "monitor event");
+    const bool ends_in_place = (sched->flags & PS_FLAG_MON_ENDS_IN_PLACE) != 0;
     // checkpoint 0: the state before the first update (asynchronous.py:181)
     int ns = 0;
-    MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
-    MCK(cudaMemcpyAsync(snaps, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, cp), "monitor snapshot");
-    MCK(cudaEventRecord(evs[0], cp), "monitor event");
+    if (ends_in_place) {
+        MCK(cudaEventRecord(evs[0], st), "monitor event");
+    } else {
+        MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
+        MCK(cudaMemcpyAsync(snaps, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, cp), "monitor snapshot");
+        MCK(cudaEventRecord(evs[0], cp), "monitor event");
+        // the solve must not start before snapshot 0 is taken
+        MCK(cudaStreamWaitEvent(st, evs[0], 0), "monitor wait");
+    }
     snap_counts[0] = 0;
     ns = 1;
-    // the solve must not start before snapshot 0 is taken
-    MCK(cudaStreamWaitEvent(st, evs[0], 0), "monitor wait");
     int r = ps_run(csr, part, prm, coord, alpha, sched, scratch, stream);
     if (r) return r;
     int64_t next_mark = every;
@@ -1875,8 +1880,9 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     // final checkpoint: after the launch (consistent)
     MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
     MCK(cudaStreamSynchronize(st), "monitor join");
-    MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, st),
-        "monitor snapshot");
+    if (!ends_in_place)
+        MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, st),
+            "monitor snapshot");
     MCK(cudaEventRecord(evs[ns], st), "monitor event");
     snap_counts[ns++] = total;
     MCK(cudaStreamSynchronize(st), "monitor join");

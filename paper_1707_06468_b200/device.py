@@ -336,8 +336,10 @@ class DeviceProblem:
         if hot is None:
             hot = self.part_kind == "singleton"
         nmax = int(-(-int(total) // int(every))) + 2
+        # checkpoint 0 and the final one are evaluated in place (below): no copies of them
         sched = self._sched(total, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta,
-                            contention=contention, hot=hot, hot_period=hot_period, flags=flags)
+                            contention=contention, hot=hot, hot_period=hot_period,
+                            flags=flags | _lib.FLAG_MON_ENDS_IN_PLACE)
         scr = self._scratch_for(sched)
         snaps = torch.empty((nmax, self.p_dev, 4), dtype=torch.float64, pin_memory=True)  # DMA targets
         counts = (ctypes.c_int64 * nmax)()
