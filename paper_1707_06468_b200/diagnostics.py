@@ -91,3 +91,54 @@ def reference_optimum(data, loss, penalty, partition, cache_dir=None, solver="de
     cache_dir.mkdir(parents=True, exist_ok=True)
     np.savez(path, x=best_x, objective=objective, residual=best_res)
     return {"x": best_x, "objective": float(objective), "residual": float(best_res), "cached": False}
+
+
+def theorem_rate_factor(n, kappa, a=1.0):
+    """Geometric rate factor of the sequential solver at step a/(5L)
+    (diagnostics.py:60-62; PAPER Theorem 1)."""
+    return 0.2 * min(1.0 / n, a / kappa)
+
+
+def theorem_constant(data, loss, xstar, L):
+    """Envelope constant ||x0 - x*||^2 + sum_i ||grad f_i(x*)||^2 / (5 L^2)
+    with x0 = 0 and zero-initialised memory (diagnostics.py:65-81).  The
+    per-sample gradients at x* are formed from the device margins; the sum
+    over i of ||l'_i a_i + lambda1 x*||^2 expands to
+    l'_i^2 ||a_i||^2 + 2 lambda1 l'_i (a_i.x*) + lambda1^2 ||x*||^2."""
+    import torch
+
+    from . import _lib
+
+    _lib.require_device()
+    f = data.features
+    ro = np.asarray(f.row_offsets, dtype=np.int64)
+    cols = np.asarray(f.col_indices, dtype=np.int64)
+    vals = np.asarray(f.values, dtype=np.float64)
+    xs = np.asarray(xstar, dtype=np.float64)
+    lens = np.diff(ro)
+    starts = np.minimum(ro[:-1], max(len(vals) - 1, 0))
+    z = np.where(lens > 0, np.add.reduceat(vals * xs[cols], starts), 0.0) if len(vals) else np.zeros(len(lens))
+    sq = np.where(lens > 0, np.add.reduceat(vals * vals, starts), 0.0) if len(vals) else np.zeros(len(lens))
+    # l'(z_i, b_i) by the library's loss code (ps_loss_deriv, the deterministic kernels' arithmetic)
+    zd = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    bd = torch.from_numpy(np.ascontiguousarray(data.labels, dtype=np.float64)).cuda()
+    out = torch.empty_like(zd)
+    _lib.check(_lib.load().ps_loss_deriv(_lib.LOSS[loss.kind], 0, zd.data_ptr(), bd.data_ptr(), zd.numel(),
+                                         out.data_ptr(), _lib.stream_ptr()))
+    deriv = out.cpu().numpy()
+    lam = loss.lambda1
+    acc = float(np.sum(deriv ** 2 * sq + 2.0 * lam * deriv * z) + data.n_samples * lam * lam * float(xs @ xs))
+    return float(xs @ xs) + acc / (5.0 * L ** 2)
+
+
+def rate_envelope_check(distance_checkpoints, rho, C0, slack):
+    """Median squared distances against (1 - rho)^t C0 slack
+    (diagnostics.py:37-57): one record per checkpoint."""
+    if not 0 < rho < 1:
+        raise ValueError("rho must be in (0, 1)")
+    records = []
+    for t, dist in sorted(distance_checkpoints.items()):
+        bound = (1.0 - rho) ** t * C0 * slack
+        records.append({"iteration": int(t), "distance": float(dist), "bound": float(bound),
+                        "passed": bool(dist <= bound), "margin": float(bound - dist)})
+    return records

@@ -218,3 +218,25 @@ def test_baseline_config2_statistics():
     assert counts.max() / f.n_rows == pytest.approx(0.963, abs=0.002)      # delta
     assert int(np.sum(counts == 0)) == pytest.approx(1142, abs=60)          # dead columns
     assert np.all(np.diff(f.col_indices.reshape(-1, 20), axis=1) > 0)
+
+
+def test_diagnostics_host_logic(tmp_path):
+    """diagnostics.py:25-62 restated: suboptimality clamps within the slack
+    and raises below it; the rate factor; envelope records."""
+    from paper_1707_06468_b200 import diagnostics as dg
+
+    assert dg.suboptimality([1.0, 0.5 + 1e-13, 0.75], 0.5) == [0.5, 1e-13 + 0.5 - 0.5, 0.25]
+    with pytest.raises(dg.StaleOptimumError):
+        dg.suboptimality([0.4], 0.5)
+    assert dg.theorem_rate_factor(200, 50.0) == pytest.approx(0.2 / 200)
+    assert dg.theorem_rate_factor(10, 50.0) == pytest.approx(0.2 / 50)
+    recs = dg.rate_envelope_check({0: 1.0, 10: 0.5, 20: 0.9}, 0.05, 1.0, 1.0)
+    assert [r["passed"] for r in recs] == [True, True, False]
+    assert recs[1]["bound"] == pytest.approx(0.95 ** 10)
+    with pytest.raises(ValueError):
+        dg.rate_envelope_check({0: 1.0}, 1.5, 1.0, 1.0)
+    d = pb.gen_sparse_glm(30, 10, 0.3, 1)
+    h1 = dg.problem_hash(d, pb.Loss("logistic", 0.1), pb.L1Penalty(0.2), pb.singleton_partition(10))
+    h2 = dg.problem_hash(d, pb.Loss("logistic", 0.1), pb.L1Penalty(0.3), pb.singleton_partition(10))
+    assert h1 != h2 and len(h1) == 64
+    assert dg.default_cache_dir().name
