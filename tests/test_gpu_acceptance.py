@@ -8,7 +8,9 @@ device solvers, with the reference's own tolerances:
       1e-8 in 120 epochs; one warp matches the sequential solver to 1e-14
       (test_acceptance.py:76-98);
 * C6  theoretical speedup >= 3 at 4 warps to 1e-6 on the near-disjoint
-      instance with delta <= 0.05 (test_acceptance.py:101-113).
+      instance with delta <= 0.05 (test_acceptance.py:101-113);
+* C7  write sparsity: no write outside the sampled extended support
+      (test_acceptance.py:116-119, verify.py:384-404).
 
 x* and F* of the acceptance instance come from the unmodified reference
 (tests/golden/ref_small.npz: reference_optimum); the speedup instance's F*
@@ -100,3 +102,28 @@ def test_criterion_6_theoretical_speedup(cuda, tmp_path):
     four = next(r for r in rows if r["cores"] == 4)
     assert index.delta <= 0.05
     assert four["reached"] and four["theoretical_speedup"] >= 3.0, rows
+
+
+@pytest.mark.parametrize("name", ["acc_l1", "grp_random"])
+def test_criterion_7_write_sparsity(cuda, name, small_cases, golden_small):
+    """verify.py:384-404: step by step over 2 epochs, the device iterate
+    changes only on the sampled row's extended support T_i (a shadow copy
+    updated on T_i stays bit-identical to x)."""
+    case = small_cases[name]
+    data, loss, part = case["data"], case["loss"], case["partition"]
+    pen = pb.L1Penalty(float(golden_small["acc__lam2"])) if name == "acc_l1" else case["penalty"]
+    dp = pb.DeviceProblem(data, loss, pen, part, drop_dead_blocks=True)
+    gamma = pb.resolve_step_size("1/5L", dp.L, data.n_samples, loss.lambda1)
+    f = data.features
+    block_of = np.asarray(part.block_of)
+    blocks = [np.flatnonzero(block_of == b) for b in range(int(block_of.max()) + 1)]
+    samples = pb.worker_rng(3, 0).integers(0, data.n_samples, size=2 * data.n_samples)
+    x = dp.x()
+    shadow = x.copy()
+    for i in samples:
+        dp.replay(np.array([i]), gamma)
+        x = dp.x()
+        cols = f.col_indices[int(f.row_offsets[i]):int(f.row_offsets[i + 1])]
+        ecols = np.unique(np.concatenate([blocks[b] for b in np.unique(block_of[cols])])) if len(cols) else cols
+        shadow[ecols] = x[ecols]
+        assert np.array_equal(x, shadow), f"write outside T_{i}"
