@@ -125,6 +125,9 @@ typedef struct ps_sched {
 /* bits 8..15: extra divisor of the staged columns' contention scale */
 #define PS_FLAG_MON_ENDS_IN_PLACE 65536 /* ps_run_monitored: skip the copies of the first and last
                                            snapshots (the caller reads coord itself) */
+#define PS_FLAG_ZERO_IMMEDIATE 131072 /* fast kernel: a staged coordinate the prox zeroes is stored by
+                                         the update itself, not by the CTA's next flush (DESIGN.md
+                                         "zero commits"; diagnostics) */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);

@@ -149,6 +149,10 @@ __device__ __forceinline__ void commit_abar(const KArgs &a, int64_t c, double in
 // (column, field) and refreshes the snapshot (~one flush per `period` CTA
 // updates).  Cuts same-sector L2 atomics on the Zipf head by ~period x.
 constexpr int NCOPY = 2;
+// staging header after the hot area (unsigned words): dirty[0..31], the
+// refresh rotation counter [32], spare [33], zero-store mask [34..65]
+constexpr int HDR_DOUBLES = 33;
+constexpr int ZMASK = 34;
 
 // shared-memory layout of the staging area (doubles):
 //   [0, 2H)            snapshot pairs (x_s, abar_s), 16 B each (cp.async target)
@@ -170,6 +174,15 @@ __device__ __forceinline__ void mark_dirty(unsigned *dirty, int slot)
     if (!(*(volatile unsigned *)w & b)) atomicOr(w, b);
 }
 
+// a staged coordinate the prox zeroed: the store x_j = 0 is issued once by the
+// CTA's next flush instead of by every update (same-address global atomics on
+// the hottest records otherwise queue at L2)
+__device__ __forceinline__ void mark_zero(unsigned *dirty, int slot)
+{
+    unsigned *w = dirty + ZMASK + (slot & 31), b = 1u << (slot >> 5);
+    if (!(*(volatile unsigned *)w & b)) atomicOr(w, b);
+}
+
 __device__ __forceinline__ double smem_take(double *p)
 {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
@@ -178,7 +191,10 @@ __device__ __forceinline__ double smem_take(double *p)
 __device__ __forceinline__ void drop_pending_x(const HotView &h, int s)
 {
 #pragma unroll
-    for (int c = 0; c < NCOPY; c++) atomicExch(reinterpret_cast<unsigned long long *>(h.pend + (2 * c) * h.H + s), 0ull);
+    for (int c = 0; c < NCOPY; c++) {
+        double *p = h.pend + (2 * c) * h.H + s;
+        if (*(volatile double *)p != 0.0) atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull);
+    }
 }
 
 // flush this CTA's pending deltas to global, then refresh the snapshot.
@@ -213,7 +229,8 @@ __device__ __noinline__ void hot_flush(const FlushArgs fa, const int H, unsigned
 {
     extern __shared__ double smem_dyn[];  // the staging area starts the dynamic shared memory
     double *pend = smem_dyn + 3 * H;
-    unsigned m = atomicExch(dirty + lane, 0u);
+    unsigned zm = atomicExch(dirty + ZMASK + lane, 0u);
+    unsigned m = atomicExch(dirty + lane, 0u) | zm;
     while (m) {
         int k = __ffs(m) - 1;
         m &= m - 1;
@@ -226,6 +243,7 @@ __device__ __noinline__ void hot_flush(const FlushArgs fa, const int H, unsigned
             dab += smem_take(pend + (2 * c + 1) * H + s);
         }
         double *g = fa.coord + 4 * hot_coord(fa, s);
+        if ((zm >> k) & 1u) atomic_exch(g, 0.0);  // deferred zero store, then the deltas added since
         if (dx != 0.0) red_add(g, dx);
         if (dab != 0.0) red_add(g + 1, dab);
     }
@@ -594,14 +612,14 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-    // shared layout: [hot staging (hot_doubles) | CTA update counter + dirty[32] (17 doubles) | per-warp scratch]
+    // shared layout: [hot staging (hot_doubles) | dirty[32] + counters + zero mask[32] (HDR_DOUBLES) | per-warp scratch]
     HotView h = hot_view(smem_dyn, a.H);
     unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
     Scratch S{};
     if constexpr (MAXT <= 256) {  // the 1024-thread variant only runs rows of <= 32 nonzeros
         if (a.stride > 0) {
-            const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
+            const int hdr = a.H > 0 ? a.hot_doubles + HDR_DOUBLES : 0;
             double *base = a.smem ? smem_dyn + hdr + (int64_t)wib * a.stride : a.gscratch + gw * a.stride;
             S = carve(base, a.M, a.GB);
         }
@@ -613,7 +631,7 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 2 * HDR_DOUBLES) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     // async work split (asynchronous.py:125-128 split_iterations): warp gw owns
@@ -858,7 +876,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 2 * HDR_DOUBLES) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     // kernel parameters used in the loop, hoisted
@@ -872,6 +890,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     const uint64_t seed = a.seed, base = a.slot_base, nrows = (uint64_t)a.n;
     const double inv_n = 1.0 / a.n_d;
     const bool store_zero = !(a.diag & PS_FLAG_DELTA_ZERO);
+    const bool zero_now = (a.diag & PS_FLAG_ZERO_IMMEDIATE) != 0;
     const int64_t nwarps = (int64_t)gridDim.x * nwib;
     const int64_t q = a.count / nwarps, rr = a.count % nwarps;
     uint64_t slot = (uint64_t)(gw * q + min(gw, rr));
@@ -988,9 +1007,16 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                     const double z = prox_t<PEN>(u, g * d[c], lam2, pen, plo, phi);
                     if (z == 0.0 && store_zero) {
                         // the prox zeroed the coordinate: commit it as a store, not as the
-                        // delta -x_hat; drops this CTA's pending delta
-                        if (sl[c] >= 0) drop_pending_x(h, sl[c]);
-                        atomic_exch(coord + 4 * (int64_t)col, 0.0);
+                        // delta -x_hat; drops this CTA's pending
+                        // delta; for a staged column the store itself is deferred to the
+                        // CTA's next flush (mark_zero)
+                        if (sl[c] >= 0) {
+                            drop_pending_x(h, sl[c]);
+                            if (zero_now) atomic_exch(coord + 4 * (int64_t)col, 0.0);
+                            else mark_zero(dirty, sl[c]);
+                        } else {
+                            atomic_exch(coord + 4 * (int64_t)col, 0.0);
+                        }
                     } else if (sl[c] >= 0) {
                         atomicAdd(px + sl[c], z - xh[c]);
                         mark_dirty(dirty, sl[c]);
@@ -1074,8 +1100,8 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
     unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
     const int HB = a.H / max(G, 1);
-    int *bcnt = reinterpret_cast<int *>(smem_dyn + a.hot_doubles + 17);
-    const int hdr = a.H > 0 ? a.hot_doubles + 17 + (HB + 1) / 2 : 0;
+    int *bcnt = reinterpret_cast<int *>(smem_dyn + a.hot_doubles + HDR_DOUBLES);
+    const int hdr = a.H > 0 ? a.hot_doubles + HDR_DOUBLES + (HB + 1) / 2 : 0;
     // per-warp staging: row value / x^ / abar^ / D per ext slot (32 * G each)
     double *wa = smem_dyn + hdr + (int64_t)wib * (4 * 32 * G);
     double *wx = wa + 32 * G, *wab = wx + 32 * G, *wd = wab + 32 * G;
@@ -1086,7 +1112,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 2 * HDR_DOUBLES) dirty[threadIdx.x] = 0u;
         for (int r = threadIdx.x; r < HB; r += blockDim.x) bcnt[r] = 0;
         __syncthreads();
     }
@@ -1318,7 +1344,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
     HotView h = hot_view(smem_dyn, a.H);
     unsigned *dirty = reinterpret_cast<unsigned *>(smem_dyn + a.hot_doubles);
     double *px = h.pend + (2 * (wib % NCOPY)) * a.H, *pab = px + a.H;
-    const int hdr = a.H > 0 ? a.hot_doubles + 17 : 0;
+    const int hdr = a.H > 0 ? a.hot_doubles + HDR_DOUBLES : 0;
     double *wa = smem_dyn + hdr + (int64_t)wib * (32 * G);  // row value per (leader lane, q)
     if (a.H > 0) {
         for (int s = threadIdx.x; s < a.H; s += blockDim.x) {
@@ -1327,7 +1353,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
             h.d[s] = __ldg(g + 2);
         }
         for (int s = threadIdx.x; s < 2 * NCOPY * a.H; s += blockDim.x) h.pend[s] = 0.0;
-        if (threadIdx.x < 34) dirty[threadIdx.x] = 0u;
+        if (threadIdx.x < 2 * HDR_DOUBLES) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
     double *const coord = a.coord;
@@ -1615,10 +1641,10 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         L->wpc = wpc = (part->G <= 5 ? 768 : 512) / 32;
         const size_t warp_stage = (size_t)wpc * 32 * part->G * 8;
         L->H -= L->H % part->G;  // whole blocks
-        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17) * 8 > 220 * 1024) L->H -= part->G;
+        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + HDR_DOUBLES) * 8 > 220 * 1024) L->H -= part->G;
         L->kernel = pick_glane(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, part->G);
         L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
-        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0);
+        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + HDR_DOUBLES) * 8 : 0);
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
         L->gscratch_bytes = 0;
@@ -1628,11 +1654,11 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         const size_t warp_stage = (size_t)wpc * 4 * 32 * part->G * 8;
         // keep the CTA within the shared-memory budget: shrink the hot set (whole blocks)
         L->H -= L->H % part->G;  // whole blocks
-        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + 17) * 8 > 220 * 1024) L->H -= part->G;
+        while (L->H > 0 && warp_stage + (size_t)((3 + 2 * NCOPY) * L->H + HDR_DOUBLES) * 8 > 220 * 1024) L->H -= part->G;
         L->kernel = pick_group(csr, prm ? prm->loss : PS_LOSS_LOGISTIC);
         L->wpc = wpc;
         L->hot_doubles = L->H > 0 ? (3 + 2 * NCOPY) * L->H : 0;
-        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0);
+        L->smem = warp_stage + (L->H > 0 ? (size_t)(L->hot_doubles + HDR_DOUBLES) * 8 : 0);
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
         L->gscratch_bytes = 0;
@@ -1649,7 +1675,7 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         if (L->fast)
             L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, part->max_slots <= 32 ? 1 : 2,
                                   wpc == FAST_T_SMALL / 32);
-        L->smem = L->H > 0 ? (size_t)(L->hot_doubles + 17) * 8 : 0;
+        L->smem = L->H > 0 ? (size_t)(L->hot_doubles + HDR_DOUBLES) * 8 : 0;
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
         L->gscratch_bytes = 0;
