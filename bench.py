@@ -118,6 +118,47 @@ def cpu_baseline(cfg, epochs=30):
             "seconds": dt, "objective": P.objective(x)}
 
 
+def cpu_baseline_big(which, n_full, epochs_to_target):
+    """the reference algorithm (oracle Hogwild port, all host
+    cores) cannot build configs 3/4 on the host; time a fixed window of 1e6
+    updates on a row-subsampled instance with the SAME p and column
+    distribution (the per-update cost depends on p and the row shape, not on
+    n), and extrapolate the time to 1e-6 from the epochs the device needed
+    (marked extrapolated)."""
+    from oracle import oracle as O
+    from paper_1707_06468_b200 import problems
+
+    rng = np.random.default_rng(100 + which)
+    n_sub = 100_000
+    if which == 3:
+        p, lam2 = 30_000_000, 1e-7
+        cols = problems.zipf_rows(rng, n_sub, p, 30, 1.2)
+        vals = np.full(cols.shape, 1.0 / np.sqrt(30))
+    else:
+        p, lam2 = 1_000_000, 1e-6
+        dense = np.broadcast_to(np.arange(13, dtype=np.int64), (n_sub, 13))
+        cols = np.concatenate([dense, problems.zipf_rows(rng, n_sub, p - 13, 22, 1.05, col_offset=13)], axis=1)
+        vals = rng.lognormal(0.0, 1.0, cols.shape)
+        vals /= np.linalg.norm(vals, axis=1, keepdims=True)
+    k = cols.shape[1]
+    y = np.where(rng.random(n_sub) < 0.5, -1.0, 1.0)
+    P = O.OracleProblem(np.arange(n_sub + 1, dtype=np.int64) * k, cols.reshape(-1), vals.reshape(-1), y, p,
+                        loss="logistic", lambda1=1.0 / n_full, penalty="l1", lam2=lam2)
+    gamma = 1.0 / (2.0 * P.lipschitz())
+    threads = os.cpu_count() or 1
+    count = 1_000_000
+    seqs = [O.sample_sequence(0, n_sub, c, worker_id=w) for w, c in enumerate(O.split_iterations(count, threads))]
+    t0 = time.perf_counter()
+    _, _, _, cnt = P.run_async(gamma, seqs)
+    dt = time.perf_counter() - t0
+    ups = cnt / dt
+    return {"value": ups, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{cnt} updates of oracle_run_async ({threads} pthreads) on a {n_sub}-row subsample with "
+                      f"config {which}'s p={p} and column distribution",
+            "time_to_1e-6_s_extrapolated": epochs_to_target * n_full / ups if epochs_to_target else None,
+            "note": "extrapolated: epochs to 1e-6 measured on the device x n / host updates/s"}
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the host cores (oracle port;
     the Python reference itself does not exist on the GPU box)."""
@@ -215,7 +256,7 @@ def lambda_path_bench(rank, world, epochs):
     return out
 
 
-def big_config_bench(which, peak):
+def big_config_bench(which, peak, with_cpu=True):
     """Full-size BASELINE config 3 / 4, generated on the device (K7): one
     launch of the config's epochs from x0 = 0, device-timed; HBM roofline from
     SURVEY §8d bytes/update (the working set does not fit L2 here)."""
@@ -269,6 +310,8 @@ def big_config_bench(which, peak):
            "bytes_per_update": bpu, "achieved_GBps": bpu * ups / 1e9, "roofline_frac": bpu * ups / 1e9 / peak,
            "objective_start": f0, "objective_end": f1, "duality_gap_end": gap1,
            "certified_rel_suboptimality_end": gap1 / abs(f1), "hot_columns": dp.H, "time_to_1e-6": ttt}
+    if with_cpu:
+        out["cpu_baseline"] = cpu_baseline_big(which, dp.n, ttt["epochs"])
     del dp, c
     torch.cuda.empty_cache()
     return out
@@ -542,7 +585,7 @@ def main():
         ingest = libsvm_bench(data)
     if world == 1 and not args.no_big:
         for which in (3, 4):
-            big[f"config{which}"] = big_config_bench(which, peak)
+            big[f"config{which}"] = big_config_bench(which, peak, with_cpu=not args.no_cpu)
 
     if rank == 0:
         line = {
