@@ -128,6 +128,9 @@ typedef struct ps_sched {
 #define PS_FLAG_ZERO_IMMEDIATE 131072 /* fast kernel: a staged coordinate the prox zeroes is stored by
                                          the update itself, not by the CTA's next flush (DESIGN.md
                                          "zero commits"; diagnostics) */
+#define PS_FLAG_GROUP_STORE_ZEROS 262144 /* lane-per-block group kernel, unstaged blocks: also store a
+                                            block that was read as zero and stays zero (default: its
+                                            zero delta is skipped; diagnostics) */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);

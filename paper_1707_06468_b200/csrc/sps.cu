@@ -1008,11 +1008,12 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
                     if (z == 0.0 && store_zero) {
                         // the prox zeroed the coordinate: commit it as a store, not as the
                         // delta -x_hat; drops this CTA's pending
-                        // delta; for a staged column the store itself is deferred to the
-                        // CTA's next flush (mark_zero)
+                        // delta.  A staged column read as 0 already: the store only undoes
+                        // other CTAs' drift, so it is deferred to the CTA's next flush
+                        // (mark_zero: one store per flush instead of one per update)
                         if (sl[c] >= 0) {
                             drop_pending_x(h, sl[c]);
-                            if (zero_now) atomic_exch(coord + 4 * (int64_t)col, 0.0);
+                            if (zero_now || xh[c] != 0.0) atomic_exch(coord + 4 * (int64_t)col, 0.0);
                             else mark_zero(dirty, sl[c]);
                         } else {
                             atomic_exch(coord + 4 * (int64_t)col, 0.0);
@@ -1359,6 +1360,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
     double *const coord = a.coord;
     double *const alpha = a.alpha;
     const double gamma = a.gamma, lambda1 = a.lambda1, kappa = a.kappa, kappa_hot = a.kappa_hot, lam2 = a.lam2;
+    const bool skip_zero = (a.diag & PS_FLAG_GROUP_STORE_ZEROS) == 0;
     const bool store_zero = !(a.diag & PS_FLAG_DELTA_ZERO);
     const uint64_t seed = a.seed, base = a.slot_base, nrows = (uint64_t)a.n;
     const double inv_n = 1.0 / a.n_d;
@@ -1457,7 +1459,14 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
                     ss += u * u;
                 }
                 const double f = group_factor(sqrt(ss), gB * d, lam2);
-                if (f == 0.0 && store_zero) {
+                bool was_zero = true;
+#pragma unroll
+                for (int q = 0; q < G; q++) was_zero = was_zero && xh[q] == 0.0;
+                if (f == 0.0 && store_zero && was_zero && skip_zero && sb < 0) {
+                    // a block read as zero that the prox keeps at zero: its delta is 0,
+                    // so nothing is committed (the store would be a same-address atomic
+                    // per coordinate on the hottest blocks; near lambda_max most of T_i)
+                } else if (f == 0.0 && store_zero) {
                     // the prox zeroed the block: store it
 #pragma unroll
                     for (int q = 0; q < G; q++) {
