@@ -131,6 +131,8 @@ typedef struct ps_sched {
 #define PS_FLAG_GROUP_STORE_ZEROS 262144 /* lane-per-block group kernel, unstaged blocks: also store a
                                             block that was read as zero and stays zero (default: its
                                             zero delta is skipped; diagnostics) */
+#define PS_FLAG_NO_CLUSTER 2097152 /* fast kernel: no CTA pairs (each CTA refreshes its hot snapshot
+                                      from L2; default: clusters of 2 share one refresh) */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);

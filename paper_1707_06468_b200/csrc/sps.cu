@@ -77,6 +77,7 @@ struct KArgs {
     int32_t hot_unit;     // coordinates per hot unit (1: columns, G: contiguous blocks)
     uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
     int32_t diag;         // ps_sched_t.flags (PS_FLAG_*)
+    int32_t cluster;      // fast kernel: CTAs per thread-block cluster (1: none)
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -218,6 +219,7 @@ __device__ __forceinline__ int64_t hot_coord(const KArgs &a, int s)
 struct FlushArgs {  // what the flush needs, by value (keeps KArgs out of local memory)
     double *coord;
     int shift, unit;
+    unsigned lead = 0u;  // shared::cluster address of the cluster leader's staging area (0: none)
 };
 __device__ __forceinline__ int64_t hot_coord(const FlushArgs &f, int s)
 {
@@ -254,6 +256,20 @@ __device__ __noinline__ void hot_flush(const FlushArgs fa, const int H, unsigned
     if (lane == 0) rot = atomicAdd(dirty + 32, 1u);
     rot = __shfl_sync(FULL, rot, 0) & 3u;
     const int kmax = (H + 31) >> 5;
+    if (fa.lead) {
+        // cluster member: refresh from the leader CTA's snapshot through
+        // distributed shared memory instead of from the hot records in L2,
+        // where the reads queue behind every CTA's REDs to the same lines
+        for (int k = 0; k < kmax; k++) {
+            int s = lane + 32 * k;
+            if (s < H && (k < HOT_TIER0 / 32 || (k & 3) == (int)rot)) {
+                double2 v;
+                asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(fa.lead + 16u * s));
+                reinterpret_cast<double2 *>(smem_dyn)[s] = v;
+            }
+        }
+        return;
+    }
     for (int k = 0; k < kmax; k++) {
         int s = lane + 32 * k;
         if (s < H && (k < HOT_TIER0 / 32 || (k & 3) == (int)rot)) {
@@ -879,6 +895,18 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         if (threadIdx.x < 2 * HDR_DOUBLES) dirty[threadIdx.x] = 0u;
         __syncthreads();
     }
+    // thread-block cluster: members refresh their hot snapshot from the
+    // leader's (rank 0), whose snapshot must be initialised first
+    unsigned lead = 0u;
+    if (a.cluster > 1) {
+        unsigned rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        if (rank != 0 && a.H > 0) {
+            const unsigned mine = (unsigned)__cvta_generic_to_shared(smem_dyn);
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead) : "r"(mine));
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     // kernel parameters used in the loop, hoisted
     double *const coord = a.coord;
     double *const alpha = a.alpha;
@@ -1035,7 +1063,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
             pnw = nw;
             prep = rep;
             if (a.H > 0 && --until_flush == 0) {
-                hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
+                hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit, lead}, a.H, dirty, lane, true);
                 until_flush = a.period;
             }
             // progress counter, bumped every PROGRESS_BATCH updates (the workers'
@@ -1063,6 +1091,8 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
         const int64_t mine = q + (gw < rr ? 1 : 0);
         if (mine % PROGRESS_BATCH) atomicAdd(a.counter, (unsigned long long)(mine % PROGRESS_BATCH));
     }
+    if (a.cluster > 1)  // the leader's staging area stays alive until every member stops reading it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (a.H > 0) {
         hot_async_drain();
         __syncthreads();
@@ -1811,8 +1841,50 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
         if (!scratch) return ps_fail(PS_EINVAL, "scratch buffer required (see ps_launch_config)");
         a.gscratch = (double *)scratch;
     }
+    // fast singleton kernel with staging: CTA pairs (thread-block clusters of 2)
+    // share the hot snapshot refresh -- the second CTA reads the first's
+    // snapshot through distributed shared memory, halving the refresh reads of
+    // the hot records at L2 (config 2: +15-20% updates/s, same epochs to 1e-6;
+    // clusters of 4 do not all fit co-resident and run at 0.65x).  Used only
+    // when every cluster of the grid can be resident at once.
+    a.cluster = 1;
+    if (L.fast && part->kind == PS_PART_SINGLETON && a.H > 0 && !(sched->flags & PS_FLAG_NO_CLUSTER) &&
+        L.ctas % 2 == 0) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(L.ctas);
+        q.blockDim = dim3(L.wpc * 32);
+        q.dynamicSmemBytes = L.smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = 2;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        int resident = 0;
+        if (cudaOccupancyMaxActiveClusters(&resident, L.kernel, &q) == cudaSuccess && 2 * resident >= L.ctas)
+            a.cluster = 2;
+        cudaGetLastError();  // a refused query leaves no sticky error behind
+    }
     void *args[] = {(void *)&a};
-    cudaError_t e = cudaLaunchKernel(L.kernel, dim3(L.ctas), dim3(L.wpc * 32), args, L.smem, (cudaStream_t)stream);
+    cudaError_t e;
+    if (a.cluster > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(L.ctas);
+        cfg.blockDim = dim3(L.wpc * 32);
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)a.cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelExC(&cfg, L.kernel, args);
+    } else {
+        e = cudaLaunchKernel(L.kernel, dim3(L.ctas), dim3(L.wpc * 32), args, L.smem, (cudaStream_t)stream);
+    }
     if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run launch");
     return PS_OK;
 }

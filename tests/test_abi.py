@@ -76,4 +76,4 @@ def test_flag_constants_match_header():
     assert defs == {"SCRAMBLE": _lib.FLAG_SCRAMBLE, "GENERIC": _lib.FLAG_GENERIC, "DELTA_ZERO": _lib.FLAG_DELTA_ZERO,
                     "GROUP_WARP": _lib.FLAG_GROUP_WARP, "GROUP_LANE": _lib.FLAG_GROUP_LANE,
                     "MON_ENDS_IN_PLACE": _lib.FLAG_MON_ENDS_IN_PLACE, "ZERO_IMMEDIATE": _lib.FLAG_ZERO_IMMEDIATE,
-                    "GROUP_STORE_ZEROS": _lib.FLAG_GROUP_STORE_ZEROS}
+                    "GROUP_STORE_ZEROS": _lib.FLAG_GROUP_STORE_ZEROS, "NO_CLUSTER": _lib.FLAG_NO_CLUSTER}
