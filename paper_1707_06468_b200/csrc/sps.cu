@@ -2004,6 +2004,12 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
         MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, st),
             "monitor snapshot");
     MCK(cudaEventRecord(evs[ns], st), "monitor event");
+    if (ends_in_place) {
+        // the last checkpoint comes after the launch AND after every snapshot copy
+        // still in flight on the copy stream (checkpoint times stay monotone)
+        MCK(cudaStreamWaitEvent(cp, evs[ns], 0), "monitor wait");
+        MCK(cudaEventRecord(evs[ns], cp), "monitor event");
+    }
     snap_counts[ns++] = total;
     MCK(cudaStreamSynchronize(st), "monitor join");
     MCK(cudaStreamSynchronize(cp), "monitor join");
