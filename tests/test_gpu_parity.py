@@ -240,12 +240,13 @@ def test_lambda_max_matches_reference_formula(cuda, small_cases):
     assert pb.lambda_max(d) == pytest.approx(expect, rel=1e-13)
 
 
-@pytest.mark.parametrize("flags", [0, 128, 32], ids=["warp_per_block", "lane_per_block", "delta_zero"])
+@pytest.mark.parametrize("flags", [0, 128, 128 | 262144, 32],
+                         ids=["warp_per_block", "lane_per_block", "lane_store_zeros", "delta_zero"])
 @pytest.mark.parametrize("name", ["grp_contig", "cfg5_small"])
 def test_async_group_kernels_converge(cuda, name, flags, small_cases, golden_small):
     """The group-lasso async kernels (the warp-cooperative default, the
-    lane-per-block one, and the reference's literal delta commit of zeroed
-    blocks) reach the deterministic solution within 1e-6 relative (grp_contig
+    lane-per-block one with and without PS_FLAG_GROUP_STORE_ZEROS, and the
+    reference's literal delta commit of zeroed blocks) reach the deterministic solution within 1e-6 relative (grp_contig
     has a ragged last block: p = 103, G = 10)."""
     case = small_cases[name]
     dp = _dp(case)
