@@ -155,15 +155,23 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
                                          hot=bool(hot) if hot is not None else False))[0]
         ctas_each = ctas if ctas > 0 else max(1, min(sms // concurrent, own))
 
+        def grid_of(k, m):
+            # the SMs left over by sms // m go to the first solves of the wave
+            # (assign() orders a rank's lambdas smallest first: the densest,
+            # slowest solves)
+            if ctas > 0 or sms // m >= own:
+                return ctas_each if m == concurrent else (ctas if ctas > 0 else max(1, min(sms // m, own)))
+            return sms // m + (1 if k < sms % m else 0)
+
         def batch(lams):
             out = []
             for w0 in range(0, len(lams), concurrent):
                 wave = lams[w0:w0 + concurrent]
                 torch.cuda.synchronize(dp.device)
-                for f, st, lam in zip(forks, streams, wave):
+                for k, (f, st, lam) in enumerate(zip(forks, streams, wave)):
                     f.lam2 = float(lam)
                     f.reset_state(stream=st)
-                    f.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=ctas_each,
+                    f.run_async(epochs * n, gamma, seed=seed, contention=contention, ctas=grid_of(k, len(wave)),
                                 warps_per_cta=warps_per_cta, flags=flags, hot=hot, stream=st)
                 torch.cuda.synchronize(dp.device)
                 for f, lam in zip(forks, wave):
