@@ -20,9 +20,11 @@ gamma = pb.resolve_step_size(c["step"], dp.L, dp.n, c["loss"].lambda1)
 dp.run_async(dp.n // 10, gamma, seed=1)
 dp.reset_state()
 t0 = time.time()
-its, objs, secs = dp.run_async_checkpointed(epochs * dp.n, dp.n, gamma, seed=3)
+import os
+hp = int(os.environ.get("HP", "0"))  # flush period override (0: library default)
+its, objs, secs = dp.run_async_checkpointed(epochs * dp.n, dp.n, gamma, seed=3, hot_period=hp)
 res = dp.fixed_point_residual(gamma)
 f, dual, gap = dp.duality_gap()
-print(json.dumps({"cfg": which, "H": dp.H, "epochs": epochs, "wall_s": time.time() - t0, "gamma": gamma, "L": dp.L,
+print(json.dumps({"cfg": which, "H": dp.H, "hp": hp, "epochs": epochs, "wall_s": time.time() - t0, "gamma": gamma, "L": dp.L,
                   "obj": [round(o, 15) for o in objs], "secs": [round(s, 5) for s in secs],
                   "residual_end": res, "gap_end": gap, "f_end": f}), flush=True)
