@@ -98,3 +98,18 @@ def test_solve_fista_and_speedup(cuda, tmp_path, capsys):
     assert lines[0] == "cores,wall_speedup,theoretical_speedup,reached"
     assert lines[1].startswith("1,1.0,1.0,true")
     assert len(list((tmp_path / "cache").glob("optimum-*.npz"))) == 1
+
+
+@pytest.mark.gpu
+def test_solve_from_libsvm_file(cuda, tmp_path, capsys):
+    """generate -> solve --data: the file goes through the device LibSVM parser
+    and the same solve as the in-memory dataset (deterministic replay)."""
+    path = tmp_path / "d.svm"
+    assert cli.main(["generate", "--synthetic", "300,40,0.1,9", "--out", str(path)]) == cli.EXIT_OK
+    capsys.readouterr()
+    assert cli.main(["solve", "--data", str(path), "--lambda2", "1e-3", "--epochs", "10", "--step", "1/2L"]) == 0
+    out = capsys.readouterr().out
+    data = pb.parse_libsvm(str(path), device=None)
+    tr = pb.run_sequential(data, pb.Loss("logistic", 1.0 / 300), pb.L1Penalty(1e-3),
+                           pb.singleton_partition(data.n_features), pb.SolverConfig(step_size="1/2L", epochs=10))
+    assert f"final objective {tr.objective[-1]:.12e}" in out

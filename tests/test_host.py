@@ -240,3 +240,22 @@ def test_diagnostics_host_logic(tmp_path):
     h2 = dg.problem_hash(d, pb.Loss("logistic", 0.1), pb.L1Penalty(0.3), pb.singleton_partition(10))
     assert h1 != h2 and len(h1) == 64
     assert dg.default_cache_dir().name
+
+
+def test_bench_first_crossing_interpolation():
+    """bench._first_crossing: log-linear interpolation of the first checkpoint
+    under the target (asynchronous.py:213-230 on the relative gap)."""
+    import math
+
+    import bench
+
+    its = [100, 200, 300]
+    walls = [1.0, 2.0, 3.0]
+    rel = [1e-4, 1e-6 * 0.1, 1e-9]
+    sec, ep = bench._first_crossing(its, walls, rel, 100, 1e-6)
+    frac = math.log(1e-4 / 1e-6) / math.log(1e-4 / 1e-7)
+    assert sec == pytest.approx(1.0 + frac) and ep == pytest.approx((100 + frac * 100) / 100)
+    assert bench._first_crossing(its, walls, [1e-3, 1e-4, 1e-5], 100, 1e-6) is None
+    # already under the target at the first checkpoint: interpolated from (0, rel 1)
+    sec, ep = bench._first_crossing([50], [0.5], [1e-8], 100, 1e-6)
+    assert 0 < sec < 0.5 and 0 < ep < 0.5
