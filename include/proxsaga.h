@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 1
+#define PS_ABI_VERSION 2
 
 enum ps_status { PS_OK = 0, PS_EINVAL = 1, PS_ERANGE = 2, PS_ECUDA = 3, PS_ENOMEM = 4 };
 /* losses.py:15-19 */
@@ -112,6 +112,14 @@ typedef struct ps_sched {
     int32_t flags;           /* PS_FLAG_* below (0 = defaults) */
     int32_t hot_shift;       /* log2 of the hot-record stride of ps_hot_layout */
     int32_t reserved;
+    /* deterministic mode only (NULL = off), p doubles each, device: per
+     * coordinate of T_i of each replayed step, the gradient estimate v of
+     * sparse_gradient_estimate (saga.py:150-166) and the applied delta z - x^
+     * (worker_iteration's return value, asynchronous.py:97-117).  The
+     * reference's step-level entry points (sps_step, worker_iteration,
+     * sparse_gradient_estimate) read them after a one-sample replay. */
+    double *trace_v;
+    double *trace_dx;
 } ps_sched_t;
 
 /* ps_sched_t.flags (async only; diagnostics except where noted) */
@@ -131,6 +139,8 @@ typedef struct ps_sched {
 #define PS_FLAG_GROUP_STORE_ZEROS 262144 /* lane-per-block group kernel, unstaged blocks: also store a
                                             block that was read as zero and stays zero (default: its
                                             zero delta is skipped; diagnostics) */
+#define PS_FLAG_FAST_V1 4194304   /* singleton fast path: the round-1 kernel (sps_fast_kernel: dirty bitmasks,
+                                      two pending copies) instead of sps_hot_kernel (A/B, diagnostics) */
 #define PS_FLAG_NO_CLUSTER 2097152 /* fast kernel: no CTA pairs (each CTA refreshes its hot snapshot
                                       from L2; default: clusters of 2 share one refresh) */
 
@@ -194,6 +204,12 @@ int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t 
  * Device pointers; an inspection / test hook for the kernels' loss code. */
 int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
                   void *stream);
+
+/* losses.py:73-86 loss_scalar, elementwise: value[i] = l(z[i], b[i]) (overflow-safe
+ * log1p forms) and deriv[i] = l'(z[i], b[i]), the deterministic kernels' arithmetic;
+ * either output may be NULL.  Device pointers. */
+int ps_loss_eval(int32_t loss, const double *z, const double *b, int64_t m, double *value, double *deriv,
+                 void *stream);
 
 /* Hot layout (SINGLETON: unit = 1, columns; CONTIG: unit = G, whole blocks):
  * units present in at least max(ceil(min_frac * n), theta) rows — theta the

@@ -25,7 +25,8 @@ PART_SINGLETON, PART_CONTIG, PART_GENERAL = 0, 1, 2
 # ps_sched_t.flags (include/proxsaga.h PS_FLAG_*)
 FLAG_SCRAMBLE, FLAG_GENERIC, FLAG_DELTA_ZERO, FLAG_GROUP_WARP, FLAG_GROUP_LANE = 4, 16, 32, 64, 128
 FLAG_MON_ENDS_IN_PLACE, FLAG_ZERO_IMMEDIATE, FLAG_GROUP_STORE_ZEROS = 65536, 131072, 262144
-FLAG_NO_CLUSTER = 2097152
+FLAG_NO_CLUSTER, FLAG_FAST_V1 = 2097152, 4194304
+ABI_VERSION = 2
 
 # Every symbol include/proxsaga.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -36,7 +37,7 @@ EXPORTS = (
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels", "ps_timestamp",
     "ps_dual_objective", "ps_run_monitored", "ps_libsvm_index", "ps_libsvm_scan", "ps_libsvm_fill",
-    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv",
+    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv", "ps_loss_eval",
 )
 
 _vp = ctypes.c_void_p
@@ -71,7 +72,8 @@ class Sched(ctypes.Structure):
     _fields_ = [("samples", _vp), ("count", _i64), ("seed", ctypes.c_uint64),
                 ("slot_base", ctypes.c_uint64), ("counter", _vp), ("batch", _i32),
                 ("ctas", _i32), ("warps_per_cta", _i32), ("hot_cols", _i32), ("contention", _f64),
-                ("hot_period", _i32), ("flags", _i32), ("hot_shift", _i32), ("reserved", _i32)]
+                ("hot_period", _i32), ("flags", _i32), ("hot_shift", _i32), ("reserved", _i32),
+                ("trace_v", _vp), ("trace_dx", _vp)]
 
 
 _P = ctypes.POINTER
@@ -110,6 +112,7 @@ def load():
         "ps_fista_prox": (_i32, [_P(Part), _P(Params), _vp, _vp, ctypes.c_double, _i64, _vp, _vp, _vp]),
         "ps_fista_extrapolate": (_i32, [_vp, _vp, ctypes.c_double, _i64, _vp, _vp]),
         "ps_loss_deriv": (_i32, [_i32, _i32, _vp, _vp, _i64, _vp, _vp]),
+        "ps_loss_eval": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp]),
         "ps_libsvm_scan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ps_libsvm_fill": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ps_run_monitored": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _vp, _P(Sched), _vp, _vp, _i64, _i32,
@@ -132,6 +135,8 @@ def load():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
+    if L.ps_abi_version() != ABI_VERSION:
+        raise LibraryMissing(f"{LIB_PATH} has ABI {L.ps_abi_version()}, this package needs {ABI_VERSION}: rebuild it")
     _lib = L
     return L
 

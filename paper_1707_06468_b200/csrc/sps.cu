@@ -78,6 +78,9 @@ struct KArgs {
     uint64_t scramble;    // diagnostics: 0, or an odd multiplier coprime to count (slot -> slot*m mod count)
     int32_t diag;         // ps_sched_t.flags (PS_FLAG_*)
     int32_t cluster;      // fast kernel: CTAs per thread-block cluster (1: none)
+    int32_t ncopy;        // sps_hot_kernel: pending-delta copies per CTA
+    // deterministic step outputs (ps_sched_t.trace_v / trace_dx), per coordinate
+    double *trace_v, *trace_dx;
     // scratch
     double *gscratch;
     int32_t stride;  // doubles per warp
@@ -391,6 +394,10 @@ __device__ __forceinline__ void row_reg(const KArgs &a, int64_t i, int64_t lo, i
             double g = slot[c] >= 0 ? a.gamma * fmin(1.0, a.kappa_hot * dr[c]) : step_of(a, dr[c]);
             double u = xr[c] - g * v;
             double z = prox_sep(a.pen, u, g * dr[c], a.lam2, a.lo, a.hi);
+            if (a.trace_v) {
+                a.trace_v[colr[c]] = v;
+                a.trace_dx[colr[c]] = z - xr[c];
+            }
             if (slot[c] >= 0 && (z != 0.0 || (a.diag & PS_FLAG_DELTA_ZERO))) {
                 atomicAdd(px + slot[c], z - xr[c]);
                 mark_dirty(dirty, slot[c]);
@@ -560,6 +567,10 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             double g = step_of(a, S.sw[s]);
             double u = xh - g * v;
             double z = prox_sep(a.pen, u, g * S.sw[s], a.lam2, a.lo, a.hi);
+            if (a.trace_v) {
+                a.trace_v[c] = v;
+                a.trace_dx[c] = z - xh;
+            }
             commit_x(a, c, xh, z);
         }
     } else if (PART == PS_PART_CONTIG) {
@@ -577,6 +588,7 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
                 xh = S.sx[s];
                 double v = S.sv[s] + ds * S.sa[s];
                 u = xh - step_of(a, dB) * v;
+                if (a.trace_v) a.trace_v[c] = v;
             }
             double sq = u * u;
 #pragma unroll
@@ -588,6 +600,7 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             if (c >= 0) {
                 double eff = step_of(a, dB) * dB;
                 double f = group_factor(sqrt(ss), eff, a.lam2);
+                if (a.trace_v) a.trace_dx[c] = u * f - xh;
                 commit_x(a, c, xh, u * f);
             }
         }
@@ -607,7 +620,12 @@ __device__ void row_slots(const KArgs &a, int64_t i, int64_t lo, int k, int lane
             for (int q = lane; q < sz; q += 32) {
                 int s = off + q;
                 double xh = S.sx[s];
-                double u = xh - gB * (S.sv[s] + ds * S.sa[s]);
+                const double v = S.sv[s] + ds * S.sa[s];
+                double u = xh - gB * v;
+                if (a.trace_v) {
+                    a.trace_v[S.si[s]] = v;
+                    a.trace_dx[S.si[s]] = u * f - xh;
+                }
                 commit_x(a, S.si[s], xh, u * f);
             }
         }
@@ -1118,6 +1136,10 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
     }
 }
 
+}  // namespace ps
+#include "fast2.cuh"
+namespace ps {
+
 // ---------------------------------------------------------------------------
 // Fast async kernel for group lasso on contiguous blocks of G <= 16
 // coordinates (BASELINE config 5), rows of <= 32 nonzeros.
@@ -1366,6 +1388,27 @@ template <typename VT, typename PT, int NC, int T> static void *kernel_ptr_fast_
 template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int loss, int pen, bool small)
 {
     return small ? kernel_ptr_fast_t<VT, PT, NC, FAST_T_SMALL>(loss, pen) : kernel_ptr_fast_t<VT, PT, NC, FAST_T>(loss, pen);
+}
+template <typename VT, typename PT, bool LIT> static void *kernel_ptr_hot_l(int loss, int pen)
+{
+    if (loss == PS_LOSS_LOGISTIC) {
+        if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, LIT>;
+        return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, LIT>;
+    }
+    if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, LIT>;
+    return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, LIT>;
+}
+template <typename VT, typename PT> static void *kernel_ptr_hot(int loss, int pen, bool literal)
+{
+    return literal ? kernel_ptr_hot_l<VT, PT, true>(loss, pen) : kernel_ptr_hot_l<VT, PT, false>(loss, pen);
+}
+static void *pick_hot(const ps_csr_t *csr, int loss, int pen, bool literal)
+{
+    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) return kernel_ptr_hot<double, long long>(loss, pen, literal);
+    if (f64) return kernel_ptr_hot<double, int>(loss, pen, literal);
+    if (i64) return kernel_ptr_hot<float, long long>(loss, pen, literal);
+    return kernel_ptr_hot<float, int>(loss, pen, literal);
 }
 // ---------------------------------------------------------------------------
 // Group lasso, lane per block (contiguous blocks of G in {2,4,5,8,10,16},
@@ -1654,9 +1697,16 @@ static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 #undef PICK
 }
 
+// pending-delta copies of sps_hot_kernel: flags bits 24..25 (0: default 2, else 1 << (v - 1))
+static int hot2_ncopy(int flags)
+{
+    const int v = (flags >> 24) & 3;
+    return v == 0 ? 2 : (1 << (v - 1));
+}
 struct LaunchCfg {
+    int ncopy = 1;
     void *kernel;
-    bool fast;
+    bool fast, hot2;
     int ctas, wpc, smem_flag, stride, M, GB, H, hot_doubles;
     size_t smem;
     int64_t gscratch_bytes;
@@ -1681,6 +1731,7 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
                           !diag_generic && (sched->warps_per_cta <= 0 || sched->warps_per_cta == FAST_T / 32 ||
                                             sched->warps_per_cta == FAST_T_SMALL / 32);
     L->H = 0;
+    L->hot2 = false;
     if (!det && (part->kind == PS_PART_SINGLETON || group_fast))
         L->H = std::min(HOT_MAX, std::max(0, (int)sched->hot_cols));
     int wpc;
@@ -1728,6 +1779,16 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
             L->kernel = pick_fast(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, part->max_slots <= 32 ? 1 : 2,
                                   wpc == FAST_T_SMALL / 32);
         L->smem = L->H > 0 ? (size_t)(L->hot_doubles + HDR_DOUBLES) * 8 : 0;
+        // second-generation hot kernel (fast2.cuh): rows <= 32 nonzeros, 32-warp CTAs
+        L->hot2 = L->fast && part->max_slots <= 32 && wpc == FAST_T / 32 && !(sched->flags & PS_FLAG_FAST_V1) &&
+                  ((sched->flags >> 8) & 0xff) == 0 && !(sched->flags & PS_FLAG_ZERO_IMMEDIATE) &&
+                  csr->n_rows < (int64_t(1) << 32);
+        if (L->hot2) {
+            L->kernel = pick_hot(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0);
+            L->ncopy = hot2_ncopy(sched->flags);
+            L->hot_doubles = L->H > 0 ? hot2_doubles(L->H, L->ncopy) : 0;
+            L->smem = (size_t)L->hot_doubles * 8 + (size_t)wpc * HOT2_BATCH_BYTES;  // + per-warp sample batches
+        }
         L->smem_flag = 0;
         L->stride = L->M = L->GB = 0;
         L->gscratch_bytes = 0;
@@ -1818,6 +1879,10 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     }
     a.slot_base = sched->slot_base;
     a.counter = sched->counter;
+    if (det && (sched->trace_v != nullptr) != (sched->trace_dx != nullptr))
+        return ps_fail(PS_EINVAL, "trace_v and trace_dx go together");
+    a.trace_v = det ? sched->trace_v : nullptr;
+    a.trace_dx = det ? sched->trace_dx : nullptr;
     a.batch = sched->batch;
     a.det = det ? 1 : 0;
 
@@ -1846,6 +1911,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
         int div = (sched->flags >> 8) & 0xff;
         a.kappa_hot = a.kappa / (double)(div > 0 ? div : 1);
     }
+    a.ncopy = L.ncopy;
     a.stride = L.stride;
     a.M = L.M;
     a.GB = L.GB;
@@ -2030,7 +2096,27 @@ __global__ void k_loss_deriv(int loss, int fast, const double *z, const double *
                                                : deriv_t<PS_LOSS_SQUARED>(z[i], b[i]);
     }
 }
+__global__ void k_loss_eval(int loss, const double *z, const double *b, int64_t m, double *val, double *der)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (val) val[i] = loss_value(loss, z[i], b[i]);
+        if (der) der[i] = loss_deriv(loss, z[i], b[i]);
+    }
+}
 }  // namespace ps
+
+extern "C" int ps_loss_eval(int32_t loss, const double *z, const double *b, int64_t m, double *value, double *deriv,
+                            void *stream)
+{
+    if (loss != PS_LOSS_LOGISTIC && loss != PS_LOSS_SQUARED) return ps_fail(PS_EINVAL, "unknown loss");
+    if (m < 0 || (m > 0 && (!z || !b || (!value && !deriv)))) return ps_fail(PS_EINVAL, "bad loss_eval arguments");
+    if (m == 0) return PS_OK;
+    ps::k_loss_eval<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(loss, z, b, m,
+                                                                                                      value, deriv);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return ps_cuda_fail(e, "ps_loss_eval launch");
+    return PS_OK;
+}
 
 extern "C" int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
                              void *stream)

@@ -17,6 +17,7 @@ streams.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 
@@ -51,7 +52,7 @@ class DeviceProblem:
 
     def __init__(self, data, loss, penalty, partition=None, device=None, drop_dead_blocks=False,
                  value_dtype="auto", hot_max=None, hot_min_frac=1.0 / 512, hot_stride=32, hot_min_rows=4096,
-                 _labels=None, _device_csr=None, _shape=None):
+                 index_dtype="auto", _labels=None, _device_csr=None, _shape=None):
         torch = _torch()
         _lib.require_device()
         self.torch = torch
@@ -89,7 +90,11 @@ class DeviceProblem:
                 def up(a):
                     return torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)
 
-                self.row_ptr_type = _lib.I32 if self.nnz < 2 ** 31 - 1 else _lib.I64
+                # int32 row pointers when they fit; index_dtype="int64" keeps the
+                # reference's own int64 (data.py:46-48) -- the PS_I64 kernels
+                if index_dtype not in ("auto", "int64"):
+                    raise ValueError("index_dtype must be 'auto' or 'int64'")
+                self.row_ptr_type = _lib.I32 if (self.nnz < 2 ** 31 - 1 and index_dtype == "auto") else _lib.I64
                 ro_d = up(f.row_offsets)
                 self.row_ptr = ro_d.to(torch.int32 if self.row_ptr_type == _lib.I32 else torch.int64)
                 self.col = up(f.col_indices).to(torch.int32)
@@ -272,11 +277,12 @@ class DeviceProblem:
         self.slot_base = 0
 
     def _sched(self, count, samples=None, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=0.0,
-               hot=True, hot_period=0, flags=0):
+               hot=True, hot_period=0, flags=0, trace=None):
+        tv, tdx = trace if trace is not None else (None, None)
         return _lib.Sched(samples, int(count), int(seed) & (2 ** 64 - 1), int(self.slot_base),
                           self.counter.data_ptr(), int(batch), int(ctas), int(warps_per_cta),
                           int(self.H if hot else 0), float(contention), int(hot_period), int(flags),
-                          int(self.hot_shift), 0)
+                          int(self.hot_shift), 0, tv, tdx)
 
     def launch_config(self, sched):
         c, w, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
@@ -292,8 +298,10 @@ class DeviceProblem:
             self._scratch = self.torch.empty((nbytes + 7) // 8, dtype=self.torch.float64, device=self.device)
         return self._scratch.data_ptr()
 
-    def replay(self, samples, gamma, stream=None):
-        """Deterministic replay of a sample sequence (saga.py:248-256) on one warp."""
+    def replay(self, samples, gamma, stream=None, trace=None):
+        """Deterministic replay of a sample sequence (saga.py:248-256) on one warp.
+        ``trace`` = (v, dx) device pointers (p doubles each): the last step's
+        gradient estimate and applied delta on its extended support."""
         torch = self.torch
         if isinstance(samples, torch.Tensor) and samples.is_cuda:
             s = samples.to(torch.int64)
@@ -303,7 +311,7 @@ class DeviceProblem:
             return
         if int(s.min()) < 0 or int(s.max()) >= self.n:
             raise IndexError("sample index out of range")
-        sched = self._sched(s.numel(), samples=s.data_ptr())
+        sched = self._sched(s.numel(), samples=s.data_ptr(), trace=trace)
         scr = self._scratch_for(sched)
         _lib.check(_lib.load().ps_run(self.csr, self.part, self.params(gamma), self.coord.data_ptr(),
                                       self.alpha.data_ptr(), sched, scr, _lib.stream_ptr(stream)))
@@ -615,3 +623,24 @@ class DeviceProblem:
             m = int(self.part.G) * g
             return 2 * s_ptr + k * (4 + s_val) + s_val + 2 * 8 + 3 * m * 8 + k * 8 + g * 8
         return 2 * s_ptr + s_val + 2 * 8 + k * (4 + s_val + 5 * 8)
+
+
+def _on_device(fn):
+    """Run a DeviceProblem method with the problem's GPU as the current device,
+    so the library (which launches on cudaGetDevice()) and the default stream
+    (torch's current stream of that device) match the state's memory."""
+
+    @functools.wraps(fn)
+    def wrapped(self, *args, **kwargs):
+        with self.torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+
+    return wrapped
+
+
+for _name in ("launch_config", "_scratch_for", "reset_state", "replay", "run_async", "run_async_monitored",
+              "run_async_checkpointed", "objective_parts", "objective", "dual_objective_dev", "duality_gap",
+              "objective_parts_of", "objective_of", "smooth_gradient_of", "fixed_point_residual",
+              "resync_average", "field", "set_x", "fork", "block_stats", "mean_blocks_per_row"):
+    setattr(DeviceProblem, _name, _on_device(getattr(DeviceProblem, _name)))
+del _name

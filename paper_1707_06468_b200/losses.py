@@ -51,19 +51,37 @@ def lipschitz_constant(data, loss, device=None):
     """Device max row norm -> L (losses.py:99-105)."""
     if data.n_samples == 0:
         raise ValueError("dataset is empty")
-    from .device import DeviceProblem
+    from . import _cache
 
-    dp = DeviceProblem.for_index(data.features, None, device=device)
+    dp = _cache.problem_for(data, loss, None, None, device=device)
     msq = float(dp.stats.max_row_sqnorm)
     return SmoothnessInfo(L=_CURVATURE[loss.kind] * msq + loss.lambda1, max_row_sqnorm=msq)
 
 
+def loss_scalar(kind, z, b):
+    """(value, derivative) of the scalar loss at margin z with label b
+    (losses.py:73-86), evaluated by the device's loss code (ps_loss_eval)."""
+    import torch
+
+    from . import _lib
+
+    if kind not in _CURVATURE:
+        raise ValueError(f"unknown loss kind {kind!r}")
+    _lib.require_device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = torch.tensor([float(z), float(b), 0.0, 0.0], dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().ps_loss_eval(_lib.LOSS[kind], t.data_ptr(), t.data_ptr() + 8, 1, t.data_ptr() + 16,
+                                        t.data_ptr() + 24, _lib.stream_ptr()))
+    out = t[2:].cpu().numpy()
+    return float(out[0]), float(out[1])
+
+
 def _problem(data, loss, penalty, partition, device):
-    from .device import DeviceProblem
+    from . import _cache
     from .penalties import ZeroPenalty
 
-    return DeviceProblem(data, loss, penalty if penalty is not None else ZeroPenalty(), partition,
-                         device=device, drop_dead_blocks=True)
+    return _cache.problem_for(data, loss, penalty if penalty is not None else ZeroPenalty(), partition,
+                              device=device)
 
 
 def full_objective(data, loss, penalty, x, partition=None, device=None):

@@ -193,16 +193,13 @@ def run_sequential(data, loss, penalty, partition, config, index=None, track_dis
     last_epoch_obj = trace.objective[0]
     done = 0
     while done < total:
+        # one replay per checkpoint segment; the tolerance test runs where the
+        # reference's does: at checkpoints that are also epoch ends (saga.py:248-256)
         nxt = min(total, (done // every + 1) * every)
-        if config.tolerance > 0:  # stop test runs at epoch boundaries
-            nxt = min(nxt, (done // n + 1) * n)
         dp.replay(samples[done:nxt], gamma)
         done = nxt
-        if done % every == 0 or done == total:
-            checkpoint(done)
+        checkpoint(done)
         if config.tolerance > 0 and done % n == 0:
-            if trace.iterations[-1] != done:
-                checkpoint(done)
             if abs(trace.objective[-1] - last_epoch_obj) < config.tolerance:
                 break
             last_epoch_obj = trace.objective[-1]
@@ -221,20 +218,20 @@ def fixed_point_residual(x, data, loss, penalty, index, gamma, device=None):
     """||x - prox_{gamma D phi}(x - gamma D grad f(x))|| on the device (saga.py:299-317)."""
     if gamma <= 0:
         raise ValueError("gamma must be positive")
-    partition = index.partition if index is not None else None
-    from .device import DeviceProblem
+    from . import _cache
 
-    dp = DeviceProblem(data, loss, penalty, partition, device=device, drop_dead_blocks=True)
+    partition = index.partition if index is not None else None
+    dp = _cache.problem_for(data, loss, penalty, partition, device=device)
     dp.set_x(x)
     return dp.fixed_point_residual(gamma)
 
 
 def resync_average(memory, data, device=None):
     """avg = A^T scalars / n on the device (saga.py:75-78)."""
-    from .device import DeviceProblem
+    from . import _cache
     from .losses import Loss
 
-    dp = DeviceProblem(data, Loss("squared"), None, None, device=device, drop_dead_blocks=True)
+    dp = _cache.problem_for(data, Loss("squared"), None, None, device=device)
     dp.alpha.copy_(dp.torch.from_numpy(np.asarray(memory.scalars, dtype=np.float64)))
     dp.resync_average()
     memory.avg[:] = dp.abar()

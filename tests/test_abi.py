@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_no_device_calls():
     L = _lib.load()
-    assert L.ps_abi_version() == 1
+    assert L.ps_abi_version() == _lib.ABI_VERSION
     assert L.ps_device_count() >= 0
 
 
@@ -43,7 +43,7 @@ def test_struct_layouts_match_header():
     # keeps 64-bit fields first so the layouts are padding-free where it matters
     assert ctypes.sizeof(_lib.Csr) == 8 * 3 + 8 * 4 + 4 * 2
     assert ctypes.sizeof(_lib.Params) == 8 + 8 * 5
-    assert ctypes.sizeof(_lib.Sched) == 8 * 5 + 4 * 4 + 8 + 4 * 4
+    assert ctypes.sizeof(_lib.Sched) == 8 * 5 + 4 * 4 + 8 + 4 * 4 + 8 * 2
 
 
 def test_solver_without_device_fails_loudly():
@@ -76,4 +76,5 @@ def test_flag_constants_match_header():
     assert defs == {"SCRAMBLE": _lib.FLAG_SCRAMBLE, "GENERIC": _lib.FLAG_GENERIC, "DELTA_ZERO": _lib.FLAG_DELTA_ZERO,
                     "GROUP_WARP": _lib.FLAG_GROUP_WARP, "GROUP_LANE": _lib.FLAG_GROUP_LANE,
                     "MON_ENDS_IN_PLACE": _lib.FLAG_MON_ENDS_IN_PLACE, "ZERO_IMMEDIATE": _lib.FLAG_ZERO_IMMEDIATE,
-                    "GROUP_STORE_ZEROS": _lib.FLAG_GROUP_STORE_ZEROS, "NO_CLUSTER": _lib.FLAG_NO_CLUSTER}
+                    "GROUP_STORE_ZEROS": _lib.FLAG_GROUP_STORE_ZEROS, "NO_CLUSTER": _lib.FLAG_NO_CLUSTER,
+                    "FAST_V1": _lib.FLAG_FAST_V1}

@@ -1,0 +1,1 @@
+timeout 300 python tools/exp_flags.py 2 30 4194304,0,67108864 2>&1 | tail -1

@@ -1,0 +1,3 @@
+set -x
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:sps_hot_kernel --launch-skip 1 -c 1 -o gpurun_out/prof_hot_v2a -f python tools/prof_async.py --batch 0 --wpc 32 --hp 24 --c 4 --per_launch 30 --hot_max 512 --warm 1 --epochs 1 > gpurun_out/prof_hot_v2a.log 2>&1
+tail -3 gpurun_out/prof_hot_v2a.log
