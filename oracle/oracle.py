@@ -143,11 +143,16 @@ class OracleProblem:
                                     len(samples), _p(x, _f64p), _p(alpha, _f64p), _p(abar, _f64p))
         return x, alpha, abar
 
-    def run_async(self, gamma, per_worker_samples, batch=100):
+    def run_async(self, gamma, per_worker_samples, batch=100, state=None):
+        """Hogwild workers from x0 = 0, or continuing ``state`` = (x, alpha, abar)
+        arrays in place (checkpointed runs)."""
         seqs = [np.ascontiguousarray(s, dtype=np.int64) for s in per_worker_samples]
         flat = np.ascontiguousarray(np.concatenate(seqs)) if seqs else np.zeros(0, np.int64)
         counts = np.array([len(s) for s in seqs], dtype=np.int64)
-        x, alpha, abar = np.zeros(self.p), np.zeros(self.n), np.zeros(self.p)
+        if state is None:
+            x, alpha, abar = np.zeros(self.p), np.zeros(self.n), np.zeros(self.p)
+        else:
+            x, alpha, abar = state
         counter = np.zeros(1, dtype=np.int64)
         lib().oracle_run_async(ctypes.byref(self._s), float(gamma), len(seqs), _p(flat, _i64p),
                                _p(counts, _i64p), _p(x, _f64p), _p(alpha, _f64p), _p(abar, _f64p),

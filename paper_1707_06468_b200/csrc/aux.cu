@@ -280,6 +280,7 @@ __global__ void k_coord_weights(double *coord, int64_t p, int kind, int G, const
 
 extern "C" int ps_prepare(const ps_csr_t *csr, ps_part_t *part, double *coord, ps_stats_t *stats, void *stream)
 {
+    NvtxRange nvtx_range("K5 ps_prepare");
     if (!csr || !part || !coord || !stats) return ps_fail(PS_EINVAL, "null argument");
     if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
     if (!part->blk_count || !part->blk_weight) return ps_fail(PS_EINVAL, "blk_count / blk_weight required");
@@ -447,6 +448,7 @@ __global__ void __launch_bounds__(256) k_objective_fused(const void *row_ptr, co
 extern "C" int ps_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
                             int32_t x_stride, double *out, void *stream)
 {
+    NvtxRange nvtx_range("K3 ps_objective");
     if (!csr || !part || !prm || !x || !out) return ps_fail(PS_EINVAL, "null argument");
     if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
     cudaStream_t st = (cudaStream_t)stream;
@@ -539,6 +541,7 @@ static int rmatvec(const ps_csr_t *csr, int loss, const double *x, int xs, const
 extern "C" int ps_smooth_gradient(const ps_csr_t *csr, const ps_params_t *prm, const double *x, int32_t x_stride,
                                   double *grad, void *stream)
 {
+    NvtxRange nvtx_range("K4 ps_smooth_gradient");
     if (!csr || !prm || !x || !grad) return ps_fail(PS_EINVAL, "null argument");
     if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
     cudaStream_t st = (cudaStream_t)stream;
@@ -551,6 +554,7 @@ extern "C" int ps_smooth_gradient(const ps_csr_t *csr, const ps_params_t *prm, c
 
 extern "C" int ps_resync_average(const ps_csr_t *csr, const double *alpha, double *coord, void *stream)
 {
+    NvtxRange nvtx_range("K4 ps_resync_average");
     if (!csr || !alpha || !coord) return ps_fail(PS_EINVAL, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
     int r = rmatvec(csr, 0, nullptr, 0, alpha, coord + 1, 4, st);
@@ -779,6 +783,7 @@ __global__ void k_dual_combine(const double *sums, const double *vmax, double in
 extern "C" int ps_dual_objective(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *x,
                                  int32_t x_stride, double *out, void *stream)
 {
+    NvtxRange nvtx_range("K8 ps_dual_objective");
     if (!csr || !part || !prm || !x || !out) return ps_fail(PS_EINVAL, "null argument");
     if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
     cudaStream_t st = (cudaStream_t)stream;
@@ -831,6 +836,7 @@ __global__ void k_sqrt(double *v) { v[0] = sqrt(v[0]); }
 extern "C" int ps_fixed_point_residual(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
                                        const double *coord, double *grad, double *out, void *stream)
 {
+    NvtxRange nvtx_range("K4 ps_fixed_point_residual");
     if (!csr || !part || !prm || !coord || !grad || !out) return ps_fail(PS_EINVAL, "null argument");
     if (!(prm->gamma > 0)) return ps_fail(PS_EINVAL, "gamma must be positive");
     cudaStream_t st = (cudaStream_t)stream;

@@ -209,15 +209,15 @@ __device__ __forceinline__ void sh_add(unsigned d, double v)
 //   [3H + 2cH, 4H + 2cH) pending x deltas, [4H + 2cH, 5H + 2cH) pending abar
 //   deltas of copy c < NC (warp w adds into copy w % NC: fewer CAS retries on
 //   the hottest slots), then H 32-bit zero-store flags and the rotation word
-//   then (16-B aligned) 1024 dirty bytes: slot s has something pending; byte
-//   (s % 32) * 32 + s / 32, so flush lane l reads its slots l, l+32, ... as
-//   32 contiguous bytes; set with plain byte stores after the pending update
+//   then (16-B aligned) 1024 dirty words, word s = slot s has something
+//   pending (set with plain 32-bit stores after the pending update; natural
+//   order keeps the hottest slots in different banks); the flush reads them
+//   four per lane per 512-B row
 __host__ __device__ constexpr unsigned hot2_dirty_off(int H, int nc)
 {
     return (8u * (3u + 2u * (unsigned)nc) * (unsigned)H + 4u * ((unsigned)H + 2u) + 15u) & ~15u;
 }
-__host__ __device__ constexpr int hot2_doubles(int H, int nc) { return (int)((hot2_dirty_off(H, nc) + 1024u + 15u) & ~15u) / 8; }
-__device__ __forceinline__ unsigned dirty_byte(unsigned s) { return ((s & 31u) << 5) | (s >> 5); }
+__host__ __device__ constexpr int hot2_doubles(int H, int nc) { return (int)((hot2_dirty_off(H, nc) + 4096u + 15u) & ~15u) / 8; }
 constexpr int HOT2_BATCH_BYTES = 0;
 
 __device__ __noinline__ void hot_flush2(double *coord, const int H, const int nc, const int shift, const unsigned lead,
@@ -227,20 +227,18 @@ __device__ __noinline__ void hot_flush2(double *coord, const int H, const int nc
     double *const pend = smem_dyn + 3 * H;
     unsigned *zf = reinterpret_cast<unsigned *>(pend + 2 * nc * H);
     const unsigned a_dirty = (unsigned)__cvta_generic_to_shared(smem_dyn) + hot2_dirty_off(H, nc);
-    // lane l flushes its dirty slots l, l + 32, ... (bytes [32 l, 32 l + 32))
-    unsigned w[8];
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                 : "r"(a_dirty + 32u * lane) : "memory");
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-                 : "r"(a_dirty + 32u * lane + 16u) : "memory");
+    // lane l flushes slots 128 r + 4 l .. + 3 of each 128-slot row r (one
+    // conflict-free 512-B read of dirty words per row)
+    for (int r0 = 0; r0 < H; r0 += 128) {
+        uint4 w;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(a_dirty + 4u * (unsigned)(r0 + 4 * lane)) : "memory");
+        const unsigned ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-        unsigned m = w[q];
-        while (m) {
-            const int byte = (__ffs(m) - 1) >> 3;
-            m &= ~(0xffu << (8 * byte));
-            const int k = 4 * q + byte, s = lane + 32 * k;
-            sh_st8(a_dirty + 32u * lane + (unsigned)k, 0u);  // cleared before the pending values are taken
+        for (int j = 0; j < 4; j++) {
+            if (!ww[j]) continue;
+            const int s = r0 + 4 * lane + j;
+            sh_st32(a_dirty + 4u * (unsigned)s, 0u);  // cleared before the pending values are taken
             double dx = 0.0, dab = 0.0;
             for (int c = 0; c < nc; c++) {
                 dx += smem_take(pend + 2 * c * H + s);
@@ -252,13 +250,13 @@ __device__ __noinline__ void hot_flush2(double *coord, const int H, const int nc
             if (dab != 0.0) red_add(g + 1, dab);
         }
     }
+    const int kmax = (H + 31) >> 5;
     if (!refresh) return;
     // tiered refresh: the HOT_TIER0 hottest slots every flush, the others a
     // rotating quarter per flush
     unsigned rot = 0;
     if (lane == 0) rot = atomicAdd(zf + H, 1u);
     rot = __shfl_sync(FULL, rot, 0) & 3u;
-    const int kmax = (H + 31) >> 5;
     if (lead) {  // cluster member: from the leader CTA's snapshot (distributed shared memory)
         for (int k = 0; k < kmax; k++) {
             const int s = lane + 32 * k;
@@ -315,7 +313,8 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
             zf[s] = 0u;
         }
         if (threadIdx.x == 0) zf[H] = 0u;
-        for (int b = threadIdx.x; b < 1024; b += blockDim.x) reinterpret_cast<unsigned char *>(smem_dyn)[hot2_dirty_off(H, nc) + b] = 0;
+        for (int b = threadIdx.x; b < 1024; b += blockDim.x)
+            reinterpret_cast<unsigned *>(reinterpret_cast<unsigned char *>(smem_dyn) + hot2_dirty_off(H, nc))[b] = 0u;
     }
     __syncthreads();
     unsigned lead = 0u;
@@ -408,7 +407,7 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
                 const double inc = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n * pval;
                 if (pcol <= -2) {
                     if (!diag_nohot) sh_add(d_pab + (unsigned)(-2 - pcol), inc);
-                    sh_st8(a_dirty + dirty_byte((unsigned)(-2 - pcol)), 1u);
+                    sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol), 1u);
                 } else if (pcol >= 0) {
                     red_add(coord + 4 * (int64_t)pcol + 1, inc);
                 }
@@ -464,7 +463,7 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
             }
             if (defer) sh_st32(a_zf + 4u * s, 1u);
             if (hot && !z0 && !diag_nohot) sh_add(d_px + s, z - xh);
-            if (hot) sh_st8(a_dirty + dirty_byte(s), 1u);  // after the pending add / zero flag (flush order)
+            if (hot) sh_st32(a_dirty + 4u * s, 1u);  // after the pending add / zero flag (flush order)
             pcol = hot ? -2 - (int)s : col;
             pval = cval;
             // ---- alpha_i <-> new (the abar credit is issued next iteration)
@@ -498,7 +497,7 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
         const double inc = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n * pval;
         if (pcol <= -2) {
             sh_add(d_pab + (unsigned)(-2 - pcol), inc);
-            sh_st8(a_dirty + dirty_byte((unsigned)(-2 - pcol)), 1u);
+            sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol), 1u);
         } else if (pcol >= 0) {
             red_add(coord + 4 * (int64_t)pcol + 1, inc);
         }
@@ -513,7 +512,7 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
         __syncthreads();
         if (wib == 0) {
             for (int b = lane; b < 1024; b += 32)
-                reinterpret_cast<unsigned char *>(smem_dyn)[hot2_dirty_off(H, nc) + b] = (((b & 31) << 5) | (b >> 5)) < H;
+                reinterpret_cast<unsigned *>(reinterpret_cast<unsigned char *>(smem_dyn) + hot2_dirty_off(H, nc))[b] = b < H;
             __syncwarp();
             hot_flush2(coord, H, nc, shift, 0u, lane, false);
         }

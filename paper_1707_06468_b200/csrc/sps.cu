@@ -718,11 +718,13 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
             hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
             until_flush = a.period;
         }
+        // progress counter, bumped every PROGRESS_BATCH updates of the warp (the
+        // workers' counter_batch, asynchronous.py:155-162): the live monitor reads it
+        if (!a.det && a.batch <= 0 && lane == 0 && ++t % PROGRESS_BATCH == 0)
+            atomicAdd(a.counter, (unsigned long long)PROGRESS_BATCH);
     }
-    if (!a.det && a.batch <= 0 && lane == 0) {  // progress counter (asynchronous.py:156-165)
-        int64_t mine = q + (gw < r ? 1 : 0);
-        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
-    }
+    if (!a.det && a.batch <= 0 && lane == 0 && t % PROGRESS_BATCH)  // the remainder
+        atomicAdd(a.counter, (unsigned long long)(t % PROGRESS_BATCH));
     if (a.H > 0) {  // every warp of the CTA has left the loop: final flush
         hot_async_drain();
         __syncthreads();
@@ -1185,6 +1187,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
     const int64_t nwarps = (int64_t)gridDim.x * nwib;
     const int64_t q0 = a.count / nwarps, rr = a.count % nwarps;
     uint64_t slot = (uint64_t)(gw * q0 + min(gw, rr));
+    int64_t prog = 0;  // this warp's updates (progress counter)
     const uint64_t slot_end = slot + (uint64_t)(q0 + (gw < rr ? 1 : 0));
     const int S = 1 << a.hot_shift;
     const int hbl = (a.H / max(G, 1)) * S;  // hot block indices are multiples of S below this
@@ -1321,15 +1324,13 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_kernel(const KArgs a)
                 hot_flush_group(a, h, bcnt, lane, true);
                 until_flush = a.period;
             }
+            if (lane == 0 && ++prog % PROGRESS_BATCH == 0) atomicAdd(a.counter, (unsigned long long)PROGRESS_BATCH);
             __syncwarp();
             if (!more) break;
             cur = nxt;
         }
     }
-    if (lane == 0) {
-        int64_t mine = q0 + (gw < rr ? 1 : 0);
-        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
-    }
+    if (lane == 0 && prog % PROGRESS_BATCH) atomicAdd(a.counter, (unsigned long long)(prog % PROGRESS_BATCH));
     if (a.H > 0) {
         hot_async_drain();
         __syncthreads();
@@ -1456,6 +1457,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
     const int64_t nwarps = (int64_t)gridDim.x * nwib;
     const int64_t q0 = a.count / nwarps, rr = a.count % nwarps;
     uint64_t slot = (uint64_t)(gw * q0 + min(gw, rr));
+    int64_t prog = 0;  // this warp's updates (progress counter)
     const uint64_t slot_end = slot + (uint64_t)(q0 + (gw < rr ? 1 : 0));
     int until_flush = a.H > 0 ? 1 + (wib * a.period) / max(1, nwib) : 0;
 
@@ -1587,6 +1589,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
                 hot_flush(FlushArgs{a.coord, a.hot_shift, a.hot_unit}, a.H, dirty, lane, true);
                 until_flush = a.period;
             }
+            if (lane == 0 && ++prog % PROGRESS_BATCH == 0) atomicAdd(a.counter, (unsigned long long)PROGRESS_BATCH);
             __syncwarp();
             if (!more) break;
             cur = nxt;
@@ -1601,10 +1604,7 @@ __global__ void __launch_bounds__(MAXT, 1) sps_group_lane_kernel(const KArgs a)
             }
         }
     }
-    if (lane == 0) {
-        int64_t mine = q0 + (gw < rr ? 1 : 0);
-        if (mine > 0) atomicAdd(a.counter, (unsigned long long)mine);
-    }
+    if (lane == 0 && prog % PROGRESS_BATCH) atomicAdd(a.counter, (unsigned long long)(prog % PROGRESS_BATCH));
     if (a.H > 0) {
         hot_async_drain();
         __syncthreads();
@@ -1697,11 +1697,11 @@ static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 #undef PICK
 }
 
-// pending-delta copies of sps_hot_kernel: flags bits 24..25 (0: default 2, else 1 << (v - 1))
+// pending-delta copies of sps_hot_kernel: flags bits 24..25 (0: default 1, else 1 << (v - 1))
 static int hot2_ncopy(int flags)
 {
     const int v = (flags >> 24) & 3;
-    return v == 0 ? 2 : (1 << (v - 1));
+    return v == 0 ? 1 : (1 << (v - 1));
 }
 struct LaunchCfg {
     int ncopy = 1;
@@ -1833,6 +1833,7 @@ extern "C" int ps_launch_config(const ps_csr_t *csr, const ps_part_t *part, cons
 extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
                       double *alpha, const ps_sched_t *sched, void *scratch, void *stream)
 {
+    NvtxRange nvtx_range("K1/K2 ps_run");
     if (!csr || !part || !prm || !coord || !alpha || !sched) return ps_fail(PS_EINVAL, "null argument");
     if (csr->n_rows < 1) return ps_fail(PS_EINVAL, "dataset is empty");
     if (!(prm->gamma > 0)) return ps_fail(PS_EINVAL, "gamma must be positive");
@@ -1984,6 +1985,7 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
                                 int32_t max_snaps, double *snaps, int64_t *snap_counts, float *snap_ms,
                                 int32_t *n_snaps)
 {
+    NvtxRange nvtx_range("K6 ps_run_monitored");
     if (!sched || !snaps || !snap_counts || !snap_ms || !n_snaps || every < 1 || max_snaps < 1)
         return ps_fail(PS_EINVAL, "bad monitor arguments");
     if (sched->samples) return ps_fail(PS_EINVAL, "the monitor is for asynchronous runs");

@@ -1,0 +1,2 @@
+timeout 300 python tools/exp_flags.py 2 30 4194304,16777216,33554432 2>&1 | tail -1
+timeout 600 python tools/exp_flags.py 3 10 4194304,16777216,33554432 2>&1 | tail -1
