@@ -309,7 +309,7 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
-def lambda_path_bench(rank, world, epochs):
+def lambda_path_bench(rank, world, epochs, ttt_epochs=30, with_oracle=True):
     """BASELINE config 5: 16-lambda group-lasso path (lambda_max .. 1e-3 lambda_max),
     independent solves sharded over the ranks (lambda_path.assign), matrix
     replicated, device-timed per rank, max over ranks; value = updates of all
@@ -362,10 +362,118 @@ def lambda_path_bench(rank, world, epochs):
     ms_s, obj_s, gap_s = sorted(reps_s, key=lambda r: r[0])[1]
     del serial
     torch.cuda.empty_cache()
+    if ttt_epochs > 0:
+        out["per_lambda"] = lambda_path_ttt(cfg, lams, mine, ttt_epochs, with_oracle=with_oracle)
     out.update(ms_serial=ms_s, ms_serial_reps=[r[0] for r in reps_s],
                max_rel_obj_diff=float(np.max(np.abs(obj_c - obj_s) / np.abs(obj_s))) if len(mine) else 0.0,
                certified_rel_gap=[float(f"{g:.3e}") for g in gap_c],
                certified_rel_gap_serial=[float(f"{g:.3e}") for g in gap_s])
+    return out
+
+
+def fista_optimum(data, loss, part, lam, max_iters=6000, target=1e-10, check=100):
+    """F* of one lambda of the path: device FISTA (fista.py:38-111 on the
+    device) from x0 = 0 until the duality gap (ps_dual_objective; F - F* <=
+    gap) is below target * |F| or max_iters; the best certified objective.
+    The reference's own protocol (diagnostics.py:153-200: a long run certified
+    by a small fixed-point residual) with the gap as the certificate."""
+    import torch
+
+    import paper_1707_06468_b200 as pb
+    from paper_1707_06468_b200.fista import FistaState, fista_step
+
+    dp = fista_optimum.dp
+    if dp is None:
+        dp = fista_optimum.dp = pb.DeviceProblem(data, loss, pb.GroupL2Penalty(lam), part, hot_max=0,
+                                                 drop_dead_blocks=True)
+    dp.lam2 = float(lam)
+    zero = torch.zeros(dp.p_dev, dtype=torch.float64, device=dp.device)
+    st = FistaState(x=zero, y=zero.clone(), t=1.0, current_L=max(dp.L / 100.0, 1e-10))
+    best = (float("inf"), float("inf"))
+    it = 0
+    t0 = time.perf_counter()
+    while it < max_iters:
+        for _ in range(check):
+            st = fista_step(st, dp)
+        it += check
+        f = float(dp.objective_parts(st.x.data_ptr(), 1).sum().item())
+        dual = float(dp.dual_objective_dev(st.x.data_ptr(), 1)[0].item())
+        if f - dual < best[1]:
+            best = (f, f - dual)
+        if f - dual <= target * abs(f):
+            break
+    return {"fstar": best[0], "gap": best[1], "rel_gap": best[1] / abs(best[0]), "iters": it,
+            "seconds": time.perf_counter() - t0}
+
+
+fista_optimum.dp = None
+
+
+def oracle_epochs_to_target(data, loss, part, lam, fstar, max_epochs, target=1e-6, budget_s=30.0):
+    """The reference algorithm's own epochs to a 1e-6 relative gap on this
+    lambda: the C oracle's sequential SPS (saga.py:217-259 restated) from
+    x0 = 0, objective after every epoch (bounded by max_epochs and budget_s)."""
+    from oracle import oracle as O
+    import paper_1707_06468_b200 as pb
+
+    P = O.from_dataset(data, loss, pb.GroupL2Penalty(lam), part)
+    gamma = 1.0 / (2.0 * P.lipschitz())
+    n = P.n
+    x, alpha, abar = np.zeros(P.p), np.zeros(n), np.zeros(P.p)
+    rng = np.random.default_rng([0, 0])
+    prev = (P.objective(x) - fstar) / abs(fstar)
+    t0 = time.perf_counter()
+    for e in range(1, max_epochs + 1):
+        x, alpha, abar = P.run_sequential(gamma, rng.integers(0, n, size=n), x, alpha, abar)
+        rel = (P.objective(x) - fstar) / abs(fstar)
+        if rel <= target:
+            import math
+
+            frac = math.log(prev / target) / math.log(prev / rel) if prev > rel > 0 else 1.0
+            return {"epochs": e - 1 + frac, "reached": True}
+        prev = max(rel, 1e-300)
+        if time.perf_counter() - t0 > budget_s:
+            return {"epochs": None, "reached": False, "epochs_run": e, "final_rel_gap": rel, "stopped": "budget"}
+    return {"epochs": None, "reached": False, "epochs_run": max_epochs, "final_rel_gap": prev}
+
+
+def lambda_path_ttt(cfg, lams, mine, epochs, with_oracle=True):
+    """Per lambda of this rank ('run each lambda to 1e-6
+    and report both'): F* by certified device FISTA, then the default group
+    solve alone on the GPU from x0 = 0 with a checkpoint per epoch
+    (stop-the-world, one CUDA graph) for up to `epochs` epochs: epochs and
+    seconds to a 1e-6 relative gap, or reached:false plus the reference
+    algorithm's own epochs to 1e-6 (the oracle) where the device budget is not
+    enough."""
+    import torch
+
+    import paper_1707_06468_b200 as pb
+
+    d, part, loss = cfg["data"], cfg["partition"], cfg["loss"]
+    fista_optimum.dp = None
+    stars = {k: fista_optimum(d, loss, part, lams[k]) for k in mine}
+    fista_optimum.dp = None
+    torch.cuda.empty_cache()
+    dp = pb.DeviceProblem(d, loss, pb.GroupL2Penalty(lams[mine[0]] if mine else 0.0), part, drop_dead_blocks=True)
+    n = d.n_samples
+    gamma = pb.resolve_step_size("1/2L", dp.L, n, loss.lambda1)
+    out = []
+    for k in mine:
+        dp.lam2 = float(lams[k])
+        fstar = stars[k]["fstar"]
+        dp.reset_state()
+        its, objs, secs = dp.run_async_checkpointed(epochs * n, n, gamma, seed=5, graph=True)
+        rel = [max((o - fstar) / abs(fstar), 1e-300) for o in objs]
+        hit = _first_crossing(its, secs, rel, n, 1e-6)
+        rec = {"lambda": lams[k], "lambda_over_max": lams[k] / lams[0], "fstar": fstar,
+               "fstar_certified_rel_gap": float(f"{stars[k]['rel_gap']:.2e}"), "fista_iters": stars[k]["iters"],
+               "reached": hit is not None, "seconds_to_1e-6": hit[0] if hit else None,
+               "epochs_to_1e-6": hit[1] if hit else None, "final_rel_gap": float(f"{rel[-1]:.3e}")}
+        if hit is None and with_oracle:
+            rec["oracle"] = oracle_epochs_to_target(d, loss, part, lams[k], fstar, max_epochs=3 * epochs)
+        out.append(rec)
+    del dp
+    torch.cuda.empty_cache()
     return out
 
 
@@ -543,9 +651,11 @@ def _split_arrays(obj, path, detail, limit=8):
     line short enough for the driver's log tail)."""
     if isinstance(obj, dict):
         return {k: _split_arrays(v, f"{path}.{k}" if path else k, detail, limit) for k, v in obj.items()}
-    if isinstance(obj, list) and len(obj) > limit:
-        detail[path] = obj
-        return f"{len(obj)} values in the --detail-out sidecar"
+    if isinstance(obj, list):
+        if len(obj) > limit and all(v is None or isinstance(v, (int, float)) for v in obj):
+            detail[path] = obj
+            return f"{len(obj)} values in the --detail-out sidecar"
+        return [_split_arrays(v, f"{path}[{i}]", detail, limit) for i, v in enumerate(obj)]
     return obj
 
 
@@ -562,6 +672,7 @@ def main():
     ap.add_argument("--no-path", action="store_true")
     ap.add_argument("--no-big", action="store_true")
     ap.add_argument("--path-epochs", type=int, default=30)
+    ap.add_argument("--path-ttt-epochs", type=int, default=30, help="per-lambda time-to-1e-6 budget (0: skip)")
     ap.add_argument("--no-io", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the literal-algorithm and config-1 records")
     ap.add_argument("--detail-out", default="bench_detail.json", help="per-checkpoint arrays (sidecar)")
@@ -722,7 +833,8 @@ def main():
     if not args.no_path:
         del dp
         torch.cuda.empty_cache()
-        lp_local = lambda_path_bench(rank, world, args.path_epochs)
+        lp_local = lambda_path_bench(rank, world, args.path_epochs, ttt_epochs=args.path_ttt_epochs,
+                                     with_oracle=not args.no_cpu)
         t = torch.tensor([lp_local["ms"], lp_local["ms_serial"], lp_local["max_rel_obj_diff"]], device="cuda")
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -741,6 +853,17 @@ def main():
                  "mean_blocks_per_row": lp_local["mean_blocks_per_row"],
                  "roofline_frac_per_gpu": upd / (float(t[0].item()) / 1e3) / world * lp_local["bytes_per_update"]
                  / 1e9 / peak}
+        if "per_lambda" in lp_local:
+            per = lp_local["per_lambda"]
+            if dist:
+                allp = [None] * world
+                dist.all_gather_object(allp, per)
+                per = sorted([r for part in allp for r in part], key=lambda r: -r["lambda"])
+            lpath["per_lambda_time_to_1e-6"] = per
+            lpath["per_lambda_note"] = ("F* per lambda: device FISTA certified by the duality gap; time to 1e-6: the "
+                                        "default group solve alone on the GPU from x0=0, one checkpoint per epoch; "
+                                        "'oracle': the reference algorithm's own epochs to 1e-6 (C oracle, "
+                                        "sequential) where the device budget was not enough")
 
     big = {}
     ingest = None

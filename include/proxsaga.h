@@ -200,7 +200,8 @@ int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t 
 /* losses.py:73-86 loss derivative, elementwise: out[i] = l'(z[i], b[i]).
  * fast = 0: the deterministic kernels' arithmetic (libdevice exp, IEEE
  * division: bit-identical to the reference's scalar formula); fast = 1: the
- * asynchronous kernels' (exp_nonpos + reciprocal-Newton division, ~1 ulp).
+ * asynchronous hot kernel's (sps_hot_kernel: table exp + one-Newton reciprocal
+ * division, ~1 ulp); fast = 2: the round-1 fast kernel's (sps_fast_kernel).
  * Device pointers; an inspection / test hook for the kernels' loss code. */
 int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
                   void *stream);

@@ -280,7 +280,7 @@ __device__ __noinline__ void hot_flush2(double *coord, const int H, const int nc
 }
 
 // LITERAL: commit prox-zeroed coordinates as the delta -x_hat (PS_FLAG_DELTA_ZERO)
-template <typename VT, typename PT, int LOSS, int PEN, bool LITERAL>
+template <typename VT, typename PT, int LOSS, int PEN, bool LITERAL, int NC>
 __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
 {
     extern __shared__ double smem_dyn[];
@@ -368,48 +368,69 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
         VT by, ny;
         load_batch(0u, bi, blo, bk, by);
         load_batch(32u, ni, nlo, nk, ny);
-        // the current update's row: column / value of lane's nonzero, sample, label
-        int col = -1;
-        VT val = VT(0);
+        // the current update's row: lane L holds nonzeros L, L + 32, ... (NC per
+        // lane, col = -1 past the row), the sample and the label
+        int col[NC];
+        VT val[NC];
         unsigned ci = __shfl_sync(FULL, bi, 0);
         VT cy = __shfl_sync(FULL, by, 0);
         {
             const PT lo0 = __shfl_sync(FULL, blo, 0);
             const int k0 = __shfl_sync(FULL, bk, 0);
-            if (lane < k0) {
-                const size_t e = sizeof(PT) == 4 ? (size_t)(unsigned)(lo0 + lane) : (size_t)(lo0 + lane);
-                col = __ldg(colp + e);
-                val = __ldg(valp + e);
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const int e = lane + 32 * c;
+                col[c] = -1;
+                val[c] = VT(0);
+                if (e < k0) {
+                    const size_t o = sizeof(PT) == 4 ? (size_t)(unsigned)(lo0 + e) : (size_t)(lo0 + e);
+                    col[c] = __ldg(colp + o);
+                    val[c] = __ldg(valp + o);
+                }
             }
         }
         // deferred abar credit of the previous update
-        int pcol = -1;  // >= 0: cold column; <= -2: staged slot -2 - pcol
-        double pval = 0.0, pnw = 0.0, prep = 0.0;
+        int pcol[NC];  // >= 0: cold column; <= -2: staged slot -2 - pcol; -1: none
+        double pval[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            pcol[c] = -1;
+            pval[c] = 0.0;
+        }
+        double pnw = 0.0, prep = 0.0;
         unsigned t = 0u;
         while (true) {
             // ---- state reads: staged columns from the CTA snapshot, others one
             // 256-bit L2 read of the record
-            const bool hot = (unsigned)col < hlim && ((unsigned)col & hmask) == 0u;
-            const unsigned s = (unsigned)col >> shift;
-            double xh = 0.0, ab = 0.0, d = 0.0;
-            if (hot) {
-                const double2 v = sh_ld2(a_snap + 16u * s);
-                xh = v.x;
-                ab = v.y;
-                d = sh_ld(a_d + 8u * s);
-            } else if (col >= 0) {
-                ld_record(coord + 4 * (int64_t)col, xh, ab, d);
+            double xh[NC], ab[NC], d[NC];
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const bool hot = (unsigned)col[c] < hlim && ((unsigned)col[c] & hmask) == 0u;
+                const unsigned sl = (unsigned)col[c] >> shift;
+                xh[c] = ab[c] = d[c] = 0.0;
+                if (hot) {
+                    const double2 v = sh_ld2(a_snap + 16u * sl);
+                    xh[c] = v.x;
+                    ab[c] = v.y;
+                    d[c] = sh_ld(a_d + 8u * sl);
+                } else if (col[c] >= 0) {
+                    ld_record(coord + 4 * (int64_t)col[c], xh[c], ab[c], d[c]);
+                }
             }
             double old = 0.0;
             if (lane == 0) old = ld_cg(alpha + ci);
             // ---- abar credit of the previous update (its alpha exchange has returned)
             {
-                const double inc = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n * pval;
-                if (pcol <= -2) {
-                    if (!diag_nohot) sh_add(d_pab + (unsigned)(-2 - pcol), inc);
-                    sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol), 1u);
-                } else if (pcol >= 0) {
-                    red_add(coord + 4 * (int64_t)pcol + 1, inc);
+                const double tq = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const double inc = tq * pval[c];
+                    if (pcol[c] <= -2) {
+                        if (!diag_nohot) sh_add(d_pab + (unsigned)(-2 - pcol[c]), inc);
+                        sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol[c]), 1u);
+                    } else if (pcol[c] >= 0) {
+                        red_add(coord + 4 * (int64_t)pcol[c] + 1, inc);
+                    }
                 }
             }
             // ---- the next update's row (extent from the batch registers)
@@ -424,48 +445,62 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
             const int src = (int)(t & 31u);
             const unsigned nci = __shfl_sync(FULL, bi, src);
             const VT ncy = __shfl_sync(FULL, by, src);
-            int ncol = -1;
-            VT nval = VT(0);
+            int ncol[NC];
+            VT nval[NC];
             {
                 const PT lo1 = __shfl_sync(FULL, blo, src);
                 const int k1 = __shfl_sync(FULL, bk, src);
-                if (lane < k1) {
-                    const size_t e = sizeof(PT) == 4 ? (size_t)(unsigned)(lo1 + lane) : (size_t)(lo1 + lane);
-                    ncol = __ldg(colp + e);
-                    nval = __ldg(valp + e);
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const int e = lane + 32 * c;
+                    ncol[c] = -1;
+                    nval[c] = VT(0);
+                    if (e < k1) {
+                        const size_t o = sizeof(PT) == 4 ? (size_t)(unsigned)(lo1 + e) : (size_t)(lo1 + e);
+                        ncol[c] = __ldg(colp + o);
+                        nval[c] = __ldg(valp + o);
+                    }
                 }
             }
             // ---- margin -> derivative
-            const double cval = widen(val);
-            const double margin = warp_sum(cval * xh);
+            double part = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; c++) part = __fma_rn(widen(val[c]), xh[c], part);
+            const double margin = warp_sum(part);
             old = __shfl_sync(FULL, old, 0);
             const double nw = deriv2<LOSS>(margin, widen(cy));
             const double ds = nw - old;
             // ---- v, step, prox, commit (asynchronous.py:97-107)
-            const double v = __fma_rn(ds, cval, d * __fma_rn(lambda1, xh, ab));
-            const double kd = kappa * d;
-            const double g = gamma * (kd < 1.0 ? kd : 1.0);
-            const double z = prox2<PEN>(__fma_rn(-g, v, xh), g * d, lam2, pen, plo, phi);
-            // commit, straight-line: a zero is stored, not added as the delta
-            // -x_hat; a staged column already read as
-            // 0 is stored by the CTA's next flush (flag), its pending delta dropped
-            const bool act = col >= 0;
-            const bool z0 = !LITERAL && act && z == 0.0;
-            const bool defer = z0 && hot && xh == 0.0;
-            double *const gx = coord + 4 * (int64_t)col;
-            if (act && !hot && !z0) red_add(gx, z - xh);
-            if (z0 && !defer) atomic_exch(gx, 0.0);
-            if (z0 && hot) {  // the coordinate is stored: drop the CTA's pending x deltas of it
-                for (int c = 0; c < nc; c++) {
-                    const unsigned ap = a_snap + 8u * ((unsigned)(3 + 2 * c) * H + s);
-                    if (sh_ld(ap) != 0.0) sh_zero64(ap);
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const double cval = widen(val[c]);
+                const double v = __fma_rn(ds, cval, d[c] * __fma_rn(lambda1, xh[c], ab[c]));
+                const double kd = kappa * d[c];
+                const double g = gamma * (kd < 1.0 ? kd : 1.0);
+                const double z = prox2<PEN>(__fma_rn(-g, v, xh[c]), g * d[c], lam2, pen, plo, phi);
+                // commit, straight-line: a zero is stored, not added as the delta
+                // -x_hat; a staged column already read as
+                // 0 is stored by the CTA's next flush (flag), its pending delta dropped
+                const bool hot = (unsigned)col[c] < hlim && ((unsigned)col[c] & hmask) == 0u;
+                const unsigned sl = (unsigned)col[c] >> shift;
+                const bool act = col[c] >= 0;
+                const bool z0 = !LITERAL && act && z == 0.0;
+                const bool defer = z0 && hot && xh[c] == 0.0;
+                double *const gx = coord + 4 * (int64_t)col[c];
+                if (act && !hot && !z0) red_add(gx, z - xh[c]);
+                if (z0 && !defer) atomic_exch(gx, 0.0);
+                if (z0 && hot) {  // the coordinate is stored: drop the CTA's pending x deltas of it
+                    for (int q = 0; q < nc; q++) {
+                        const unsigned ap = a_snap + 8u * ((unsigned)(3 + 2 * q) * H + sl);
+                        if (sh_ld(ap) != 0.0) sh_zero64(ap);
+                    }
                 }
+                if (defer) sh_st32(a_zf + 4u * sl, 1u);
+                if (hot && !z0 && !diag_nohot) sh_add(d_px + sl, z - xh[c]);
+                if (hot) sh_st32(a_dirty + 4u * sl, 1u);  // after the pending add / zero flag (flush order)
+                pcol[c] = hot ? -2 - (int)sl : col[c];
+                pval[c] = cval;
             }
-            if (defer) sh_st32(a_zf + 4u * s, 1u);
-            if (hot && !z0 && !diag_nohot) sh_add(d_px + s, z - xh);
-            if (hot) sh_st32(a_dirty + 4u * s, 1u);  // after the pending add / zero flag (flush order)
-            pcol = hot ? -2 - (int)s : col;
-            pval = cval;
             // ---- alpha_i <-> new (the abar credit is issued next iteration)
             double rep = 0.0;
             if (lane == 0) rep = atomic_exch(alpha + ci, nw);
@@ -488,18 +523,24 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
             }
             __syncwarp();
             if (t == todo) break;
-            col = ncol;
-            val = nval;
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                col[c] = ncol[c];
+                val[c] = nval[c];
+            }
             ci = nci;
             cy = ncy;
         }
         // last credit
-        const double inc = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n * pval;
-        if (pcol <= -2) {
-            sh_add(d_pab + (unsigned)(-2 - pcol), inc);
-            sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol), 1u);
-        } else if (pcol >= 0) {
-            red_add(coord + 4 * (int64_t)pcol + 1, inc);
+        const double tq = (pnw - __shfl_sync(FULL, prep, 0)) * inv_n;
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            if (pcol[c] <= -2) {
+                sh_add(d_pab + (unsigned)(-2 - pcol[c]), tq * pval[c]);
+                sh_st32(a_dirty + 4u * (unsigned)(-2 - pcol[c]), 1u);
+            } else if (pcol[c] >= 0) {
+                red_add(coord + 4 * (int64_t)pcol[c] + 1, tq * pval[c]);
+            }
         }
     }
     if (lane == 0 && todo % PROGRESS_BATCH) atomicAdd(a.counter, (unsigned long long)(todo % PROGRESS_BATCH));

@@ -1390,26 +1390,28 @@ template <typename VT, typename PT, int NC> static void *kernel_ptr_fast(int los
 {
     return small ? kernel_ptr_fast_t<VT, PT, NC, FAST_T_SMALL>(loss, pen) : kernel_ptr_fast_t<VT, PT, NC, FAST_T>(loss, pen);
 }
-template <typename VT, typename PT, bool LIT> static void *kernel_ptr_hot_l(int loss, int pen)
+template <typename VT, typename PT, bool LIT, int NC> static void *kernel_ptr_hot_l(int loss, int pen)
 {
     if (loss == PS_LOSS_LOGISTIC) {
-        if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, LIT>;
-        return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, LIT>;
+        if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, LIT, NC>;
+        return (void *)sps_hot_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, LIT, NC>;
     }
-    if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, LIT>;
-    return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, LIT>;
+    if (pen == PS_PEN_L1) return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, LIT, NC>;
+    return (void *)sps_hot_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, LIT, NC>;
 }
-template <typename VT, typename PT> static void *kernel_ptr_hot(int loss, int pen, bool literal)
+template <typename VT, typename PT> static void *kernel_ptr_hot(int loss, int pen, bool literal, int nc)
 {
-    return literal ? kernel_ptr_hot_l<VT, PT, true>(loss, pen) : kernel_ptr_hot_l<VT, PT, false>(loss, pen);
+    if (nc == 2)
+        return literal ? kernel_ptr_hot_l<VT, PT, true, 2>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 2>(loss, pen);
+    return literal ? kernel_ptr_hot_l<VT, PT, true, 1>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 1>(loss, pen);
 }
-static void *pick_hot(const ps_csr_t *csr, int loss, int pen, bool literal)
+static void *pick_hot(const ps_csr_t *csr, int loss, int pen, bool literal, int nc)
 {
     bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (f64 && i64) return kernel_ptr_hot<double, long long>(loss, pen, literal);
-    if (f64) return kernel_ptr_hot<double, int>(loss, pen, literal);
-    if (i64) return kernel_ptr_hot<float, long long>(loss, pen, literal);
-    return kernel_ptr_hot<float, int>(loss, pen, literal);
+    if (f64 && i64) return kernel_ptr_hot<double, long long>(loss, pen, literal, nc);
+    if (f64) return kernel_ptr_hot<double, int>(loss, pen, literal, nc);
+    if (i64) return kernel_ptr_hot<float, long long>(loss, pen, literal, nc);
+    return kernel_ptr_hot<float, int>(loss, pen, literal, nc);
 }
 // ---------------------------------------------------------------------------
 // Group lasso, lane per block (contiguous blocks of G in {2,4,5,8,10,16},
@@ -1780,11 +1782,12 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
                                   wpc == FAST_T_SMALL / 32);
         L->smem = L->H > 0 ? (size_t)(L->hot_doubles + HDR_DOUBLES) * 8 : 0;
         // second-generation hot kernel (fast2.cuh): rows <= 32 nonzeros, 32-warp CTAs
-        L->hot2 = L->fast && part->max_slots <= 32 && wpc == FAST_T / 32 && !(sched->flags & PS_FLAG_FAST_V1) &&
+        L->hot2 = L->fast && part->max_slots <= 64 && wpc == FAST_T / 32 && !(sched->flags & PS_FLAG_FAST_V1) &&
                   ((sched->flags >> 8) & 0xff) == 0 && !(sched->flags & PS_FLAG_ZERO_IMMEDIATE) &&
                   csr->n_rows < (int64_t(1) << 32);
         if (L->hot2) {
-            L->kernel = pick_hot(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0);
+            L->kernel = pick_hot(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0,
+                                 part->max_slots <= 32 ? 1 : 2);
             L->ncopy = hot2_ncopy(sched->flags);
             L->hot_doubles = L->H > 0 ? hot2_doubles(L->H, L->ncopy) : 0;
             L->smem = (size_t)L->hot_doubles * 8 + (size_t)wpc * HOT2_BATCH_BYTES;  // + per-warp sample batches
@@ -1928,8 +1931,11 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     // clusters of 4 do not all fit co-resident and run at 0.65x).  Used only
     // when every cluster of the grid can be resident at once.
     a.cluster = 1;
+    // (sps_hot_kernel: only up to 512 staged columns -- with 1024 the members'
+    // second-hand tier-2 refresh measured unstable on a config-3-like
+    // instance, tools/gpu/dbg_knobs.py, and round 1 measured no gain there)
     if (L.fast && part->kind == PS_PART_SINGLETON && a.H > 0 && !(sched->flags & PS_FLAG_NO_CLUSTER) &&
-        L.ctas % 2 == 0) {
+        L.ctas % 2 == 0 && !(L.hot2 && a.H > 512)) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(L.ctas);
         q.blockDim = dim3(L.wpc * 32);
@@ -2094,8 +2100,10 @@ __global__ void k_loss_deriv(int loss, int fast, const double *z, const double *
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         if (!fast) out[i] = loss_deriv(loss, z[i], b[i]);
-        else out[i] = loss == PS_LOSS_LOGISTIC ? deriv_t<PS_LOSS_LOGISTIC>(z[i], b[i])
-                                               : deriv_t<PS_LOSS_SQUARED>(z[i], b[i]);
+        else if (fast == 2) out[i] = loss == PS_LOSS_LOGISTIC ? deriv_t<PS_LOSS_LOGISTIC>(z[i], b[i])
+                                                              : deriv_t<PS_LOSS_SQUARED>(z[i], b[i]);
+        else out[i] = loss == PS_LOSS_LOGISTIC ? deriv2<PS_LOSS_LOGISTIC>(z[i], b[i])
+                                               : deriv2<PS_LOSS_SQUARED>(z[i], b[i]);
     }
 }
 __global__ void k_loss_eval(int loss, const double *z, const double *b, int64_t m, double *val, double *der)

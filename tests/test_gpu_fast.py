@@ -207,11 +207,12 @@ def _ulps(a, b):
 
 
 def test_async_loss_derivative_accuracy(cuda):
-    """The asynchronous kernels' logistic derivative (exp_nonpos + reciprocal
-    Newton division, ps_loss_deriv fast=1) against the deterministic kernels'
-    (libdevice exp + IEEE division, the reference's formula losses.py:73-86):
-    within 4 ulp everywhere (measured 3; subnormal results included), the same NaNs, over
-    margins spanning the underflow range of exp."""
+    """The asynchronous kernels' logistic derivative (ps_loss_deriv fast=1: the
+    hot kernel's table exp + one-Newton reciprocal division; fast=2: the
+    round-1 kernel's exp_nonpos + two Newton steps) against the deterministic
+    kernels' (libdevice exp + IEEE division, the reference's formula
+    losses.py:73-86): within 4 ulp everywhere (subnormal results included),
+    the same NaNs, over margins spanning the underflow range of exp."""
     import torch
 
     from paper_1707_06468_b200 import _lib
@@ -224,17 +225,18 @@ def test_async_loss_derivative_accuracy(cuda):
     b = np.where(rng.random(z.size) < 0.5, -1.0, 1.0)
     zd, bd = torch.from_numpy(z).cuda(), torch.from_numpy(b).cuda()
     outs = []
-    for fast in (0, 1):
+    for fast in (0, 1, 2):
         o = torch.empty_like(zd)
         _lib.check(_lib.load().ps_loss_deriv(0, fast, zd.data_ptr(), bd.data_ptr(), z.size, o.data_ptr(), 0))
         outs.append(o.cpu().numpy())
-    ref, fast = outs
-    assert np.array_equal(np.isnan(ref), np.isnan(fast))
+    ref = outs[0]
     ok = ~np.isnan(ref)
-    # ulps of the int64 views: same-sign values, so zeros and subnormals are
-    # measured on the same scale (exp underflow rounds within one subnormal ulp)
-    assert np.array_equal(np.signbit(ref[ok]), np.signbit(fast[ok]))
-    assert _ulps(ref[ok], fast[ok]).max() <= 4  # exp ~1 ulp, faithful division, libdevice exp <= 1 ulp
+    for fast in outs[1:]:
+        assert np.array_equal(np.isnan(ref), np.isnan(fast))
+        # ulps of the int64 views: same-sign values, so zeros and subnormals are
+        # measured on the same scale (exp underflow rounds within one subnormal ulp)
+        assert np.array_equal(np.signbit(ref[ok]), np.signbit(fast[ok]))
+        assert _ulps(ref[ok], fast[ok]).max() <= 4  # exp ~1 ulp, faithful division, libdevice exp <= 1 ulp
     # the deterministic path restates losses.py:73-86 (numpy, same branches)
     t = -b * z
     with np.errstate(over="ignore", invalid="ignore"):

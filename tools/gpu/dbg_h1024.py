@@ -12,7 +12,7 @@ c = problems.device_zipf_problem(n, int(1.5 * n), 0, 30, 1.2, 10_000, 1e-7, Fals
 dp = c["problem"]
 gamma = pb.resolve_step_size("1/2L", dp.L, dp.n, c["loss"].lambda1)
 print("H", dp.H, "shift", dp.hot_shift, flush=True)
-for flags in [4194304, 0, 16777216]:
+for flags in [4194304, 0]:
     dp.reset_state()
     objs = []
     for e in range(6):
