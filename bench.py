@@ -196,17 +196,17 @@ def config1_bench():
 def literal_bench(dp, gamma, total, n, fstar):
     """The reference's literal ProxASAGA on the device: plain step gamma
     (contention = 0) and prox-zeroed coordinates committed as the delta -x^
-    (PS_FLAG_DELTA_ZERO), at the largest number of warps in flight (148 CTAs
-    x {32, 8, 4, 2, 1} warps) whose 30-epoch solve reaches a 1e-6 relative
-    gap; updates/s and time to 1e-6 (stop-the-world per-epoch checkpoints)
-    beside the default.  Hot columns stay staged per CTA (write-combining of
-    the same per-update arithmetic)."""
+    (PS_FLAG_DELTA_ZERO), at the largest number of warps in flight (the full
+    staged grid, then 592 .. 1 unstaged warps) whose 30-epoch solve reaches a
+    1e-6 relative gap; updates/s and time to 1e-6 (stop-the-world per-epoch
+    checkpoints) beside the default."""
     from paper_1707_06468_b200 import _lib
     import torch
 
     tried = []
     best = None
-    for ctas, wpc, hot in ((148, 32, True), (148, 8, True), (148, 4, True), (148, 2, True), (148, 1, True)):
+    for ctas, wpc, hot in ((148, 32, True), (148, 4, False), (148, 1, False), (74, 1, False), (37, 1, False),
+                           (16, 1, False), (8, 1, False), (4, 1, False), (2, 1, False), (1, 1, False)):
         kw = dict(ctas=ctas, warps_per_cta=wpc, contention=0.0, hot=hot, flags=_lib.FLAG_DELTA_ZERO)
         dp.reset_state()
         its, objs, secs = dp.run_async_checkpointed(total, n, gamma, seed=21, graph=True, **kw)
@@ -344,16 +344,36 @@ def lambda_path_bench(rank, world, epochs, ttt_epochs=30, with_oracle=True):
         return (s.elapsed_time(e), np.array([r["objective"] for r in res]),
                 np.array([r["gap"] / abs(r["objective"]) for r in res]))
 
+    # the rank's lambdas in ONE lambda-batched launch (ps_batch_run: every
+    # sampled row applied to all B states; B = the rank's lambda count rounded
+    # up to a power of two, <= 16)
+    B = 1
+    while B < min(16, max(1, len(mine))):
+        B *= 2
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", batched=B)
+    solve.batch([lams[k] for k in mine])  # warm-up
+    reps_c = [timed(solve) for _ in range(3)]
+    ms_c, obj_c, gap_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
+    dpb = solve.batched.dp
+    s_ptr, s_val = (4 if dpb.row_ptr_type == 0 else 8), (4 if dpb.value_type == 0 else 8)
+    kbar = dpb.nnz / dpb.n
+    row_bytes = 2 * s_ptr + kbar * (4 + s_val) + s_val  # the CSR row + label, read once per B states
+    bpu_b = dpb.bytes_per_update() - (1.0 - 1.0 / B) * row_bytes
+    out.update(ms=ms_c, ms_reps=[r[0] for r in reps_c], batched=B, bytes_per_update=bpu_b,
+               bytes_per_update_unbatched=dpb.bytes_per_update(), mean_blocks_per_row=dpb.mean_blocks_per_row())
+    del solve
+    torch.cuda.empty_cache()
+    # the round-1 schedule beside it: the rank's lambdas as concurrent forks
     conc = max(1, len(mine))
     solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=conc)
     if solve.batch is not None:
-        solve.batch([lams[k] for k in mine])  # warm-up
+        solve.batch([lams[k] for k in mine])
     else:
         solve(lams[mine[0]] if mine else lams[0])
-    reps_c = [timed(solve) for _ in range(3)]
-    ms_c, obj_c, gap_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
-    out.update(ms=ms_c, ms_reps=[r[0] for r in reps_c], concurrent=conc,
-               bytes_per_update=solve.problem.bytes_per_update(), mean_blocks_per_row=solve.problem.mean_blocks_per_row())
+    reps_k = [timed(solve) for _ in range(3)]
+    ms_k = sorted(r[0] for r in reps_k)[1]
+    out.update(ms_concurrent=ms_k, concurrent=conc,
+               certified_rel_gap_concurrent=[float(f"{g:.3e}") for g in sorted(reps_k, key=lambda r: r[0])[1][2]])
     del solve
     torch.cuda.empty_cache()
     serial = lp.device_solver(d, loss, part, epochs=epochs, mode="async", concurrent=1)
@@ -835,7 +855,8 @@ def main():
         torch.cuda.empty_cache()
         lp_local = lambda_path_bench(rank, world, args.path_epochs, ttt_epochs=args.path_ttt_epochs,
                                      with_oracle=not args.no_cpu)
-        t = torch.tensor([lp_local["ms"], lp_local["ms_serial"], lp_local["max_rel_obj_diff"]], device="cuda")
+        t = torch.tensor([lp_local["ms"], lp_local["ms_serial"], lp_local["max_rel_obj_diff"],
+                          lp_local["ms_concurrent"]], device="cuda")
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         upd = 16 * args.path_epochs * 100_000
@@ -843,10 +864,13 @@ def main():
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
                  "value": upd / (float(t[0].item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t[0].item()),
+                 "schedule": f"lambda-batched kernel, B={lp_local['batched']} states per launch per rank",
+                 "concurrent_value": upd / (float(t[3].item()) / 1e3),
                  "concurrent_per_rank": lp_local["concurrent"], "rank0_ms_reps": lp_local["ms_reps"],
+                 "rank0_certified_rel_gap_per_lambda_concurrent": lp_local["certified_rel_gap_concurrent"],
                  "rank0_serial_ms_reps": lp_local["ms_serial_reps"],
                  "serial_value": upd / (float(t[1].item()) / 1e3),
-                 "max_rel_objective_diff_concurrent_vs_serial": float(t[2].item()),
+                 "max_rel_objective_diff_batched_vs_serial": float(t[2].item()),
                  "rank0_certified_rel_gap_per_lambda": lp_local["certified_rel_gap"],
                  "rank0_certified_rel_gap_per_lambda_serial": lp_local["certified_rel_gap_serial"],
                  "n_gpus": world, "algorithmic_bytes_per_update": lp_local["bytes_per_update"],

@@ -206,6 +206,23 @@ int ps_prox(const ps_params_t *prm, const double *v, const double *eff, int64_t 
 int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, int64_t m, double *out,
                   void *stream);
 
+/* Lambda-batched group-lasso SPS (a regularisation path, BASELINE config 5):
+ * B in {1,2,4,8,16} solves of the same problem that differ only in the group
+ * weight lam2[beta] (device, B doubles; prm->lam2 is ignored), sharing each
+ * sampled row: saga.py:150-185 / asynchronous.py:80-117 per state.  State:
+ * NB*G*B*2 doubles (NB = ceil(p/G)), coordinate j of state beta at
+ * (((beta/S)*NB*G + j)*S + beta%S)*2 + {0: x, 1: abar} with S = min(B, 2)
+ * (use ps_batch_field); alpha[i*B + beta]; d_B from ps_prepare (part->blk_weight).
+ * CONTIG partitions of G <= 16, rows <= 32 nonzeros, int32 row pointers.
+ * sched->samples != NULL: deterministic replay of the sequence on one warp
+ * (every state takes the same samples); else asynchronous, one warp per
+ * in-flight row (sched->counter counts rows). */
+int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
+                 int32_t B, double *state, double *alpha, const ps_sched_t *sched, void *stream);
+/* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state) */
+int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
+                   int32_t set, void *stream);
+
 /* losses.py:73-86 loss_scalar, elementwise: value[i] = l(z[i], b[i]) (overflow-safe
  * log1p forms) and deriv[i] = l'(z[i], b[i]), the deterministic kernels' arithmetic;
  * either output may be NULL.  Device pointers. */

@@ -2,13 +2,16 @@
 
 ``run_async`` keeps the reference's signature and trace contract
 (asynchronous.py:131-210).  The reference's Python worker threads become
-resident warps of one persistent kernel (ps_run, async mode): each warp
-claims ``counter_batch`` sample slots at a time from a device counter (the
-reference's batched iteration counter, :156-165), draws its rows from an
-on-device counter-based sampler, reads x / abar inconsistently from L2 and
-commits with atomicAdd / atomicExch.  The monitor (:187-198) becomes a
-host loop that launches one kernel per checkpoint segment and evaluates the
-objective on the device between segments.
+resident warps of one persistent kernel (ps_run, async mode): the call's
+sample slots are split statically over the warps (the reference's
+split_iterations, :125-128), each warp draws its rows from an on-device
+counter-based sampler, reads x / abar inconsistently and commits with REDs /
+atomic exchanges (hot columns through per-CTA staging).  The monitor
+(:187-198) is the live one: ONE launch for the whole solve, a progress
+counter bumped every 16 updates of a warp, and at each checkpoint mark a
+copy-engine snapshot of the running solve (ps_run_monitored); the
+stop-the-world schedule (one launch per segment) remains for snapshots that
+would not fit in host memory and for distance tracking.
 
 ``config.threads == 1`` replays worker 0's reference sample stream on a single
 warp, so a 1-thread run equals ``run_sequential`` bit for bit, as in the
@@ -56,10 +59,19 @@ def split_iterations(total, threads):
 
 
 def _grid(dp, config):
+    """(ctas, warps_per_cta) launching exactly config.warps warps: warps per CTA
+    = the largest divisor of the count up to 8 (one CTA of all of them up to
+    32), unless warps_per_cta is given (then ctas * wpc may round down)."""
     if config.warps is None:
         return 0, config.warps_per_cta
-    wpc = config.warps_per_cta or min(8, config.warps)
-    return max(1, config.warps // wpc), wpc
+    w = int(config.warps)
+    if config.warps_per_cta:
+        wpc = int(config.warps_per_cta)
+    elif w <= 32:
+        wpc = w
+    else:
+        wpc = max(d for d in range(1, 9) if w % d == 0)
+    return max(1, w // wpc), wpc
 
 
 def run_async(data, loss, penalty, partition, config, index=None, track_distance_to=None, max_threads=64,
@@ -76,7 +88,9 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
     meta["counter_batch"] = config.counter_batch
     ctas, wpc = _grid(dp, config)
     if config.threads > 1:
-        c, w, _ = dp.launch_config(dp._sched(1, batch=config.counter_batch, ctas=ctas, warps_per_cta=wpc))
+        # the grid the launches below use (static split, batch 0; hot staging as run_async_monitored picks)
+        c, w, _ = dp.launch_config(dp._sched(1, batch=0, ctas=ctas, warps_per_cta=wpc,
+                                             hot=dp.part_kind == "singleton"))
         meta["warps_in_flight"] = c * w
     trace = Trace(meta=meta)
     track = track_distance_to is not None
@@ -157,7 +171,7 @@ def measure_speedup(data, loss, penalty, partition, config, cores, target_subopt
         run_cfg = AsyncConfig(step_size=config.step_size, epochs=config.epochs, seed=config.seed,
                               checkpoint_every=config.checkpoint_every, tolerance=0.0,
                               threads=min(c, 2) if c > 1 else 1, counter_batch=config.counter_batch,
-                              warps=c if c > 1 else None, warps_per_cta=min(8, c) if c > 1 else 0)
+                              warps=c if c > 1 else None, warps_per_cta=0)
         trace = run_async(data, loss, penalty, partition, run_cfg, device=device)
         traces[c] = trace
         hit = iterations_to_target(trace, fstar, target_subopt)

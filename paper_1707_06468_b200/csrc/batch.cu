@@ -1,0 +1,353 @@
+// Lambda-batched group-lasso SPS (BASELINE config 5; SURVEY §8(e) "Option").
+//
+// B independent solves of the same problem that differ only in the penalty
+// weight (a regularisation path) share every sampled row: one warp reads row
+// i once -- the sample, the CSR extent, its columns / values / label, its
+// distinct blocks T_i -- and applies the Sparse Proximal SAGA step
+// (saga.py:150-185 / asynchronous.py:80-117, group prox penalties.py:103-108)
+// to all B lambda-states.  The per-sample scalar work (margin reduction,
+// logistic derivative, alpha exchange) runs once per lane for B states in
+// parallel instead of once per warp per state.
+//
+// State layout (bidx below): states in groups of 2, each group its own
+// region [block][q][2](x, abar); alpha[i*B + beta]; the block weights d_B
+// come from ps_prepare (part->blk_weight).
+//
+// Lane mapping: LPB = 32/B lanes per state; lane l works on state l % B and
+// on the block coordinates q = l / B + LPB r.  Rows of <= 32 nonzeros,
+// contiguous blocks of G <= 16.  Asynchronous mode: one warp per in-flight
+// row, REDs on x / abar, atomicExch on alpha (asynchronous.py's atomics);
+// deterministic mode (sched->samples): one warp, plain stores in sps_step's
+// order (x = x^ + (z - x^), abar += ((new - alpha_i)/n) a_i, alpha_i = new).
+#include <algorithm>
+#include <cstdio>
+
+#include "fastmath.cuh"
+#include "internal.h"
+
+namespace ps {
+
+struct BArgs {
+    const int32_t *row_ptr;
+    const int32_t *col;
+    const void *val, *y;
+    int64_t n, p;
+    int32_t G;
+    const double *bd;   // d_B per block
+    double *state;      // see above
+    double *alpha;      // [n][B]
+    const double *lam2; // [B]
+    int32_t loss;
+    double lambda1, gamma, kappa, n_d;
+    int64_t nb;  // blocks (ceil(p / G))
+    // schedule
+    const int64_t *samples;
+    int64_t count;
+    uint64_t seed, slot_base;
+    unsigned long long *counter;
+    int32_t det, skip_zero;
+};
+
+constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
+// State layout: states are grouped S = 2 at a time (one 32-B sector per
+// coordinate and group); group g of the B states is its own region
+//   state[((g * NB*G + j) * S + beta % S) * 2 + {0: x, 1: abar}],  g = beta / S
+// so a block's B states sit in B/S regions (hundreds of MB apart): the REDs
+// of a hot block -- every row updates the Zipf head's blocks -- reach B/S
+// times more L2 slices than one contiguous [b][q][beta] record (ncu: one
+// slice's atomic unit 88% busy with the contiguous record, 20.5 M rows/s
+// whatever the grid; 22.2 M with the groups), at the same sectors per warp
+// access.  A region per (group, q) (G*B/S regions) spreads them further but
+// measured slower (16.2 M rows/s: each lane's loads of a block land in
+// different 2 MB pages).
+constexpr int BATCH_S = 2;
+constexpr int PROGRESS_BATCH_B = 16;           // rows per progress bump of a warp
+constexpr int BATCH_SM_WARP = 32 + 32 * 16;    // per-warp shared doubles: block ids + row values [32][16]
+__host__ __device__ __forceinline__ int64_t bidx(int64_t j, int beta, int64_t nb, int G, int S)
+{
+    return (((int64_t)(beta / S) * nb * G + j) * S + beta % S) * 2;
+}
+
+template <typename VT, int LOSS, int B, int GT>
+__global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
+{
+    constexpr int LPB = 32 / B;                                  // lanes per state
+    constexpr int S = B < BATCH_S ? B : BATCH_S;                 // states per layout group
+    constexpr int RMAX = ((GT > 0 ? GT : 16) + LPB - 1) / LPB;   // block coordinates per lane
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int nwib = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * nwib + wib;
+    const int beta = lane % B, sub = lane / B;
+    int *sblk = reinterpret_cast<int *>(smem_dyn + (size_t)wib * BATCH_SM_WARP);
+    double *sa = smem_dyn + (size_t)wib * BATCH_SM_WARP + 32;  // [rank][16]
+    const int G = GT > 0 ? GT : a.G;
+    const int64_t p = a.p;
+    double *const st = a.state;
+    const double lam2 = a.lam2[beta];
+    const VT *valp = reinterpret_cast<const VT *>(a.val);
+    const VT *yp = reinterpret_cast<const VT *>(a.y);
+
+    const int64_t nwarps = (int64_t)gridDim.x * nwib;
+    int64_t t0, t1;
+    if (a.det) {
+        if (gw != 0) return;
+        t0 = 0;
+        t1 = a.count;
+    } else {
+        const int64_t q = a.count / nwarps, r = a.count % nwarps;
+        t0 = gw * q + min(gw, r);
+        t1 = t0 + q + (gw < r ? 1 : 0);
+    }
+    int64_t done = 0;
+    for (int64_t t = t0; t < t1; t++) {
+        const int64_t i = a.det ? __ldg(a.samples + t) : sample_row(a.seed, a.slot_base + (uint64_t)t, (uint64_t)a.n);
+        const int lo = __ldg(a.row_ptr + i), k = __ldg(a.row_ptr + i + 1) - lo;
+        // ---- the row's nonzeros (lane e) and distinct blocks (ranks)
+        int col = -1;
+        double val = 0.0;
+        if (lane < k) {
+            col = __ldg(a.col + lo + lane);
+            val = widen(__ldg(valp + lo + lane));
+        }
+        const double yb = widen(__ldg(yp + i));
+        double old = 0.0;  // alpha_i of this lane's state (lanes < B)
+        if (sub == 0) old = a.det ? a.alpha[i * B + beta] : ld_cg(a.alpha + i * B + beta);
+        // margin loads issued first: x[col_e][beta] for this lane's nonzeros e = sub + LPB j
+        double xm[(32 + LPB - 1) / LPB];
+#pragma unroll
+        for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
+            const int e = sub + LPB * j;
+            const int ce = __shfl_sync(FULL, col, e & 31);
+            xm[j] = (e < k) ? ld_cg(st + bidx(ce, beta, a.nb, G, S)) : 0.0;
+        }
+        const int blk = col >= 0 ? col / G : -1 - lane;
+        const unsigned peers = __match_any_sync(FULL, blk);
+        const int lead = __ffs(peers) - 1;
+        const unsigned leaders = __ballot_sync(FULL, col >= 0 && lead == lane);
+        const int g = __popc(leaders);
+        const int rank = __popc(leaders & ((1u << lead) - 1u));
+        for (int s = lane; s < g * 16; s += 32) sa[s] = 0.0;
+        __syncwarp();
+        if (col >= 0) {
+            sa[rank * 16 + (col - blk * G)] = val;
+            if (lead == lane) sblk[rank] = blk;
+        }
+        __syncwarp();
+        // block weights of T_i: lane t holds d_B of rank t
+        double dB = 0.0;
+        if (lane < g) dB = __ldg(a.bd + sblk[lane]);
+        // ---- margins
+        double part = 0.0;
+#pragma unroll
+        for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
+            const int e = sub + LPB * j;
+            const double ve = __shfl_sync(FULL, val, e & 31);
+            part = __fma_rn(ve, xm[j], part);  // xm = 0 past the row
+        }
+#pragma unroll
+        for (int o = B; o < 32; o <<= 1) part += __shfl_xor_sync(FULL, part, o);
+        old = __shfl_sync(FULL, old, beta);
+        const double nw = LOSS == PS_LOSS_LOGISTIC ? deriv2<PS_LOSS_LOGISTIC>(part, yb) : part - yb;
+        const double ds = nw - old;
+        // alpha_i <- new now (the exchange returns while the blocks are updated)
+        double rep = old;
+        if (sub == 0) {
+            if (a.det) a.alpha[i * B + beta] = nw;
+            else rep = atomic_exch(a.alpha + i * B + beta, nw);
+        }
+        // ---- every block of T_i, all B states; the next block's state loads
+        // are issued before the current block is computed
+        double2 cur[RMAX];
+        auto load_blk = [&](int tb, double2 *v) {
+            const int b = sblk[tb];
+            const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) {
+                const int q = sub + LPB * r;
+                v[r] = q < nq ? ld_cg2(st + bidx((int64_t)b * G + q, beta, a.nb, G, S)) : make_double2(0.0, 0.0);
+            }
+        };
+        if (g > 0) load_blk(0, cur);
+        for (int tb = 0; tb < g; tb++) {
+            double2 nxt[RMAX];
+            if (tb + 1 < g) load_blk(tb + 1, nxt);
+            const int b = sblk[tb];
+            const double d = __shfl_sync(FULL, dB, tb);
+            const double kd = a.kappa * d;
+            const double gB = a.gamma * (kd < 1.0 ? kd : 1.0);
+            const int nq = (int)min((int64_t)G, p - (int64_t)b * G);
+            double u[RMAX];
+            double ss = 0.0;
+            bool zero = true;
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) {
+                const int q = sub + LPB * r;
+                u[r] = 0.0;
+                if (q < nq) {
+                    const double vv = __fma_rn(ds, sa[tb * 16 + q], d * __fma_rn(a.lambda1, cur[r].x, cur[r].y));
+                    u[r] = __fma_rn(-gB, vv, cur[r].x);
+                    ss = __fma_rn(u[r], u[r], ss);
+                    zero = zero && cur[r].x == 0.0;
+                }
+            }
+#pragma unroll
+            for (int o = B; o < 32; o <<= 1) {
+                ss += __shfl_xor_sync(FULL, ss, o);
+                zero = (__shfl_xor_sync(FULL, (int)zero, o) != 0) && zero;
+            }
+            const double f = group_factor(sqrt(ss), gB * d, lam2);
+            // zero block kept at zero: delta 0, nothing committed (the lane
+            // kernel's skip); a zeroed block is stored (zero commits)
+            if (!(f == 0.0 && zero && a.skip_zero)) {
+#pragma unroll
+                for (int r = 0; r < RMAX; r++) {
+                    const int q = sub + LPB * r;
+                    if (q < nq) {
+                        double *px = st + bidx((int64_t)b * G + q, beta, a.nb, G, S);
+                        const double z = u[r] * f;
+                        if (a.det) *px = cur[r].x + (z - cur[r].x);
+                        else if (f == 0.0) atomic_exch(px, 0.0);
+                        else red_add(px, z - cur[r].x);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) cur[r] = nxt[r];
+        }
+        // ---- abar on S_i: ((new - replaced)/n) a_i
+        rep = __shfl_sync(FULL, rep, beta);
+        const double tq = (nw - rep) / a.n_d;  // saga.py:182-184: (delta / n) * vals
+        for (int e0 = 0; e0 < k; e0 += LPB) {
+            const int e = e0 + sub;
+            const int ce = __shfl_sync(FULL, col, e & 31);
+            const double ve = __shfl_sync(FULL, val, e & 31);
+            if (e < k) {
+                double *pab = st + bidx(ce, beta, a.nb, G, S) + 1;
+                if (a.det) *pab = *pab + tq * ve;
+                else red_add(pab, tq * ve);
+            }
+        }
+        if (a.det) {
+            __threadfence();
+        } else if (lane == 0 && ++done % PROGRESS_BATCH_B == 0) {
+            atomicAdd(a.counter, (unsigned long long)PROGRESS_BATCH_B);
+        }
+        __syncwarp();
+    }
+    if (!a.det && lane == 0 && done % PROGRESS_BATCH_B) atomicAdd(a.counter, (unsigned long long)(done % PROGRESS_BATCH_B));
+}
+
+template <typename VT, int LOSS, int GT> static void *pick_bg(int B)
+{
+    switch (B) {
+    case 1: return (void *)sps_group_batch_kernel<VT, LOSS, 1, GT>;
+    case 2: return (void *)sps_group_batch_kernel<VT, LOSS, 2, GT>;
+    case 4: return (void *)sps_group_batch_kernel<VT, LOSS, 4, GT>;
+    case 8: return (void *)sps_group_batch_kernel<VT, LOSS, 8, GT>;
+    default: return (void *)sps_group_batch_kernel<VT, LOSS, 16, GT>;
+    }
+}
+// G = 10 (BASELINE config 5) specialised, other G <= 16 at runtime
+template <typename VT, int LOSS> static void *pick_b(int B, int G)
+{
+    return G == 10 ? pick_bg<VT, LOSS, 10>(B) : pick_bg<VT, LOSS, 0>(B);
+}
+
+__global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G, int B, int beta, int field,
+                              double *out, int set)
+{
+    const int S = B < BATCH_S ? B : BATCH_S;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        double *s = const_cast<double *>(state) + bidx(j, beta, nb, G, S) + field;
+        if (set) *s = out[j];
+        else out[j] = *s;
+    }
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
+                            int32_t B, double *state, double *alpha, const ps_sched_t *sched, void *stream)
+{
+    NvtxRange nvtx_range("K2b ps_batch_run");
+    if (!csr || !part || !prm || !lam2 || !state || !alpha || !sched) return ps_fail(PS_EINVAL, "null argument");
+    if (B != 1 && B != 2 && B != 4 && B != 8 && B != 16) return ps_fail(PS_EINVAL, "B must be 1, 2, 4, 8 or 16");
+    if (part->kind != PS_PART_CONTIG || part->G < 1 || part->G > 16 || !part->blk_weight)
+        return ps_fail(PS_EINVAL, "batched path: contiguous blocks of G <= 16 with ps_prepare weights");
+    if (part->max_row_nnz > 32) return ps_fail(PS_EINVAL, "batched path: rows of <= 32 nonzeros");
+    if (csr->row_ptr_type != PS_I32) return ps_fail(PS_EINVAL, "batched path: int32 row pointers");
+    if (prm->penalty != PS_PEN_GROUP) return ps_fail(PS_EINVAL, "batched path: group penalty");
+    if (!(prm->gamma > 0)) return ps_fail(PS_EINVAL, "gamma must be positive");
+    if (sched->count < 0) return ps_fail(PS_EINVAL, "negative update count");
+    if (sched->count == 0) return PS_OK;
+    const bool det = sched->samples != nullptr;
+    if (!det && !sched->counter) return ps_fail(PS_EINVAL, "async mode needs a device counter");
+    BArgs a{};
+    a.row_ptr = static_cast<const int32_t *>(csr->row_ptr);
+    a.col = csr->col_idx;
+    a.val = csr->values;
+    a.y = csr->labels;
+    a.n = csr->n_rows;
+    a.p = csr->n_cols;
+    a.G = part->G;
+    a.bd = part->blk_weight;
+    a.state = state;
+    a.alpha = alpha;
+    a.lam2 = lam2;
+    a.loss = prm->loss;
+    a.lambda1 = prm->lambda1;
+    a.gamma = prm->gamma;
+    a.n_d = (double)csr->n_rows;
+    a.nb = (csr->n_cols + part->G - 1) / part->G;
+    a.samples = sched->samples;
+    a.count = sched->count;
+    {  // splitmix64(seed), host side (as ps_run)
+        uint64_t z = sched->seed + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        a.seed = z ^ (z >> 31);
+    }
+    a.slot_base = sched->slot_base;
+    a.counter = sched->counter;
+    a.det = det ? 1 : 0;
+    a.skip_zero = (sched->flags & PS_FLAG_GROUP_STORE_ZEROS) ? 0 : 1;
+    void *kern;
+    const bool f64 = csr->value_type == PS_F64, sq = prm->loss == PS_LOSS_SQUARED;
+    const int G = part->G;
+    if (f64) kern = sq ? pick_b<double, PS_LOSS_SQUARED>(B, G) : pick_b<double, PS_LOSS_LOGISTIC>(B, G);
+    else kern = sq ? pick_b<float, PS_LOSS_SQUARED>(B, G) : pick_b<float, PS_LOSS_LOGISTIC>(B, G);
+    const int wpc = sched->warps_per_cta > 0 ? std::min(sched->warps_per_cta, BATCH_T / 32) : BATCH_T / 32;
+    const size_t smem = (size_t)wpc * BATCH_SM_WARP * 8;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                             "ps_batch_run smem attribute");
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, smem), "ps_batch_run occupancy");
+    // default grid: one full wave, but no more than n/16 rows in flight (as ps_run)
+    const int64_t cap = std::max<int64_t>(1, csr->n_rows / (16 * (int64_t)wpc));
+    const int ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas
+                                                : (int)std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), cap));
+    // per-coordinate step damping as ps_run: tau = rows in flight (every state sees all of them)
+    const double tau = (double)ctas * wpc;
+    a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
+    void *args[] = {(void *)&a};
+    CK(cudaLaunchKernel(kern, dim3(ctas), dim3(wpc * 32), args, smem, (cudaStream_t)stream), "ps_batch_run launch");
+    return PS_OK;
+}
+
+extern "C" int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
+                              int32_t set, void *stream)
+{
+    if (!state || !vec || beta < 0 || beta >= B || field < 0 || field > 1 || G < 1) return ps_fail(PS_EINVAL, "bad argument");
+    if (p <= 0) return PS_OK;
+    const int64_t nb = (p + G - 1) / G;
+    k_batch_field<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(state, p, nb, G, B,
+                                                                                                  beta, field, vec, set);
+    CK(cudaGetLastError(), "ps_batch_field launch");
+    return PS_OK;
+}

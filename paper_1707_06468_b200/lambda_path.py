@@ -100,7 +100,7 @@ def _summary(dp, updates):
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
                   mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0, concurrent=1,
-                  flags=0, hot=None):
+                  flags=0, hot=None, batched=0):
     """A ``solve(lam)`` closure over one DeviceProblem (uploaded once).
 
     ``concurrent`` > 1 (async mode): ``solve.batch(lams)`` runs that many
@@ -137,6 +137,24 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
     solve.problem = dp
     solve.gamma = gamma
     solve.batch = None
+    if batched > 0 and penalty_kind == "group" and samples is None:
+        # lambda-batched kernel: `batched` states per launch share each sampled row
+        bp = BatchedPath(data, loss, partition, B=batched, device=device)
+        bgamma = resolve_step_size(step, bp.dp.L, n, loss.lambda1 if loss.lambda1 > 0 else None)
+
+        def batch(lams):
+            out = []
+            for w0 in range(0, len(lams), batched):
+                wave = list(lams[w0:w0 + batched])
+                bp.reset(wave)
+                bp.run(epochs * n, bgamma, seed=seed, contention=contention, ctas=ctas, warps_per_cta=warps_per_cta)
+                for beta in range(len(wave)):
+                    out.append(bp.summary(beta, epochs * n, keep_x=keep_x))
+            return out
+
+        solve.batch = batch
+        solve.batched = bp
+        return solve
     if concurrent > 1 and samples is None:
         # concurrent group solves: the lane-per-block kernel (fewer instructions
         # per update; with 1/concurrent of the SMs per state its hot blocks no
@@ -187,6 +205,101 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
     return solve
 
 
+class BatchedPath:
+    """B lambda-solves of one group-lasso problem advanced together by the
+    lambda-batched kernel (ps_batch_run): one warp per sampled row applies the
+    step to all B states, so the sample, the CSR row and the per-row scalar
+    work are shared.  State layout [block][q][beta](x, abar) on the device,
+    alpha [n][beta]; the problem (CSR, partition, d_B) is the DeviceProblem's,
+    uploaded once (no hot-unit renumbering: blocks keep their ids)."""
+
+    def __init__(self, data, loss, partition, B=16, device=None, dp=None):
+        from .device import DeviceProblem
+        from .penalties import GroupL2Penalty
+
+        if B not in (1, 2, 4, 8, 16):
+            raise ValueError("B must be 1, 2, 4, 8 or 16")
+        self.dp = dp if dp is not None else DeviceProblem(data, loss, GroupL2Penalty(0.0), partition, device=device,
+                                                          drop_dead_blocks=True, hot_max=0)
+        if self.dp.perm is not None:
+            raise ValueError("the batched path needs the natural block layout (hot_max=0)")
+        torch = self.torch = self.dp.torch
+        self.B = B
+        dev = self.dp.device
+        with torch.cuda.device(dev):
+            G = int(self.dp.part.G)
+            self.state = torch.zeros(-(-self.dp.p_dev // G) * G * B * 2, dtype=torch.float64, device=dev)
+            self.alpha = torch.zeros(self.dp.n * B, dtype=torch.float64, device=dev)
+            self.lam2 = torch.zeros(B, dtype=torch.float64, device=dev)
+            self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.vec = torch.empty(self.dp.p_dev, dtype=torch.float64, device=dev)
+        self.slot_base = 0
+
+    def reset(self, lams):
+        """x0 = 0, abar = 0, alpha = 0 for every state; lam2[beta] = lams[beta]
+        (fewer lambdas than B: the spare states repeat the last one)."""
+        lams = list(lams)
+        if not 1 <= len(lams) <= self.B:
+            raise ValueError("between 1 and B lambdas")
+        self.lams = lams
+        vals = lams + [lams[-1]] * (self.B - len(lams))
+        with self.torch.cuda.device(self.dp.device):
+            self.state.zero_()
+            self.alpha.zero_()
+            self.lam2.copy_(self.torch.tensor(vals, dtype=self.torch.float64))
+        self.slot_base = 0
+
+    def run(self, rows, gamma, seed=0, contention=4.0, ctas=0, warps_per_cta=0, samples=None, stream=None):
+        """`rows` sampled rows, each applied to every state (asynchronous), or
+        the deterministic replay of `samples` (one warp)."""
+        from . import _lib
+
+        dp = self.dp
+        with self.torch.cuda.device(dp.device):
+            ptr = None
+            if samples is not None:
+                s = self.torch.from_numpy(np.ascontiguousarray(samples, dtype=np.int64)).to(dp.device)
+                ptr, rows, self._keep = s.data_ptr(), int(s.numel()), s
+            else:
+                self.counter.zero_()
+            sched = _lib.Sched(ptr, int(rows), int(seed) & (2 ** 64 - 1), int(self.slot_base), self.counter.data_ptr(),
+                               0, int(ctas), int(warps_per_cta), 0, float(contention), 0, 0, 0, 0, None, None)
+            _lib.check(_lib.load().ps_batch_run(dp.csr, dp.part, dp.params(gamma), self.lam2.data_ptr(), self.B,
+                                                self.state.data_ptr(), self.alpha.data_ptr(), sched,
+                                                _lib.stream_ptr(stream)))
+            if samples is None:
+                self.slot_base += int(rows)
+
+    def field(self, beta, f=0):
+        """x (f=0) or abar (f=1) of state beta as a device p-vector."""
+        from . import _lib
+
+        with self.torch.cuda.device(self.dp.device):
+            out = self.torch.empty(self.dp.p_dev, dtype=self.torch.float64, device=self.dp.device)
+            _lib.check(_lib.load().ps_batch_field(self.state.data_ptr(), self.dp.p_dev, int(self.dp.part.G), self.B,
+                                                  int(beta), int(f), out.data_ptr(), 0, _lib.stream_ptr()))
+        return out
+
+    def summary(self, beta, updates, keep_x=False):
+        """Objective, Fenchel dual and gap (a certificate), nnz and norm of state beta."""
+        from . import _lib
+
+        dp = self.dp
+        x = self.field(beta)
+        saved = dp.lam2
+        dp.lam2 = float(self.lams[beta])
+        with self.torch.cuda.device(dp.device):
+            parts = dp.objective_parts(x.data_ptr(), 1).cpu().numpy()
+            dual = float(dp.dual_objective_dev(x.data_ptr(), 1)[0].item())
+        dp.lam2 = saved
+        obj = float(parts.sum())
+        out = {"objective": obj, "dual": dual, "gap": obj - dual, "nnz": int((x != 0).sum().item()),
+               "norm": float(self.torch.linalg.vector_norm(x).item()), "updates": updates}
+        if keep_x:
+            out["x"] = x.cpu().numpy()
+        return out
+
+
 def lambda_max_for(data, partition, penalty_kind="group", device=None):
     from .problems import group_lambda_max, lambda_max
 
@@ -196,13 +309,14 @@ def lambda_max_for(data, partition, penalty_kind="group", device=None):
 
 
 def regularization_path(data, loss, partition, n_lambdas=16, ratio=1e-3, penalty_kind="group", epochs=30,
-                        step="1/2L", seed=0, mode="async", device=None, keep_x=False, concurrent=1):
+                        step="1/2L", seed=0, mode="async", device=None, keep_x=False, concurrent=1, batched=0):
     """Config 5 end to end on this rank's GPU (call under torchrun for N GPUs).
-    ``concurrent`` lambdas of this rank's share run at a time (device_solver)."""
+    ``batched`` = B > 0: the rank's lambdas B at a time through the
+    lambda-batched kernel; else ``concurrent`` lambdas at a time as forks."""
     lam_max = lambda_max_for(data, partition, penalty_kind, device=device)
     lams = lambda_grid(lam_max, n_lambdas, ratio)
     solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
-                          keep_x=keep_x, concurrent=concurrent)
+                          keep_x=keep_x, concurrent=concurrent, batched=batched)
     t0 = time.perf_counter()
     res = run_path(lams, solve)
     return {"lambda_max": lam_max, "lambdas": lams, "results": res, "seconds": time.perf_counter() - t0,

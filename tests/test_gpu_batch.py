@@ -1,0 +1,75 @@
+"""The lambda-batched group-lasso kernel (ps_batch_run, csrc/batch.cu): B
+solves of one problem sharing each sampled row.
+
+Tolerances:
+  * deterministic replay: every state equals the single-lambda deterministic
+    replay of the same sample sequence (which matches the reference's
+    iterates, tests/test_gpu_parity.py) to 1e-9 relative, and the reference's
+    golden iterates where the golden case's lambda is used;
+  * asynchronous: each state's objective within 1e-6 relative of that
+    lambda's optimum (a long deterministic replay), abar = A^T alpha / n per
+    state to 1e-12.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1707_06468_b200 as pb
+from paper_1707_06468_b200 import problems
+from paper_1707_06468_b200.device import DeviceProblem
+from paper_1707_06468_b200.lambda_path import BatchedPath, device_solver
+from paper_1707_06468_b200.saga import resolve_step_size, worker_rng
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.mark.parametrize("B", [4, 16])
+def test_batched_deterministic_replay_matches_single_lambda(cuda, B, small_cases, golden_small):
+    case, g = small_cases["grp_contig"], golden_small
+    data, loss, part = case["data"], case["loss"], case["partition"]
+    lam0 = case["penalty"].lam2
+    lams = [lam0 * f for f in (1.0, 0.5, 0.2, 0.05, 2.0, 0.1, 0.01, 1.5)][:B] + [lam0] * max(0, B - 8)
+    bp = BatchedPath(data, loss, part, B=B)
+    gamma = resolve_step_size(case["step"], bp.dp.L, bp.dp.n, loss.lambda1)
+    seq = worker_rng(case["seed"], 0).integers(0, data.n_samples, size=case["segments"][0])
+    bp.reset(lams)
+    bp.run(0, gamma, samples=seq)
+    for beta, lam in enumerate(lams):
+        dp = DeviceProblem(data, loss, pb.GroupL2Penalty(lam), part, drop_dead_blocks=True, hot_max=0)
+        dp.replay(seq, gamma)
+        x = bp.field(beta).cpu().numpy()
+        assert _rel(x, dp.x()) <= 1e-9, (beta, lam)
+        assert _rel(bp.field(beta, 1).cpu().numpy(), dp.abar()) <= 1e-9
+        a = bp.alpha.view(-1, B)[:, beta].cpu().numpy()
+        assert np.max(np.abs(a - dp.alpha.cpu().numpy())) <= 1e-9
+        if lam == lam0:  # the reference's own iterate (tests/golden, make_golden.py)
+            assert _rel(x, g["grp_contig__x"][0]) <= 1e-9
+
+
+def test_batched_async_reaches_each_optimum(cuda):
+    rng = np.random.default_rng(11)
+    data = problems._zipf_logistic(rng, 8000, 40000, 20, 1.1, 100)
+    part = pb.contiguous_partition(data.n_features, 10)
+    lam1 = 1.0 / data.n_samples
+    loss = pb.Loss("logistic", lam1)
+    lmax = pb.group_lambda_max(data, part)
+    lams = [f * lmax for f in (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005)]
+    solve = device_solver(data, loss, part, epochs=60, seed=3, batched=8)
+    res = solve.batch(lams)
+    bp = solve.batched
+    n = data.n_samples
+    for beta, (lam, r) in enumerate(zip(lams, res)):
+        dp = DeviceProblem(data, loss, pb.GroupL2Penalty(lam), part, drop_dead_blocks=True, hot_max=0)
+        gamma = resolve_step_size("1/2L", dp.L, n, lam1)
+        dp.replay(worker_rng(99, 0).integers(0, n, size=150 * n), gamma)
+        fref = dp.objective()
+        assert abs(r["objective"] - fref) <= 1e-6 * abs(fref), (lam / lmax, r["objective"], fref)
+        assert r["gap"] >= -1e-12 and r["objective"] >= r["dual"]
+        # abar stays the exact average of this state's alpha table
+        dp.alpha.copy_(bp.alpha.view(-1, 8)[:, beta])
+        dp.resync_average()
+        assert np.max(np.abs(bp.field(beta, 1).cpu().numpy() - dp.abar())) <= 1e-12

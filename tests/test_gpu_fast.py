@@ -282,3 +282,26 @@ def _abar_exact(dp):
     dp.coord.copy_(keep)
     assert live.shape == exact.shape
     return exact
+
+
+@pytest.mark.parametrize("kind", ["generic_warps4", "group_contig"])
+def test_live_monitor_sees_every_epoch(cuda, kind):
+    """run_async under the live monitor records one checkpoint per epoch on
+    every kernel (the generic and group kernels bump the progress counter
+    every 16 updates of a warp, as the fast kernels do)."""
+    data = _instance(20, n=20000)
+    lam = 1.0 / data.n_samples
+    epochs = 6
+    if kind == "generic_warps4":
+        pen, part = pb.L1Penalty(lam), pb.singleton_partition(data.n_features)
+        cfg = pb.AsyncConfig(step_size="1/2L", epochs=epochs, seed=1, threads=2, warps=4)
+    else:
+        pen, part = pb.GroupL2Penalty(lam), pb.contiguous_partition(data.n_features, 10)
+        cfg = pb.AsyncConfig(step_size="1/2L", epochs=epochs, seed=1, threads=2)
+    tr = pb.run_async(data, pb.Loss("logistic", lam), pen, part, cfg)
+    assert len(tr.iterations) == epochs + 1, tr.iterations
+    n = data.n_samples
+    assert tr.iterations[0] == 0 and tr.iterations[-1] == epochs * n
+    assert all(b > a for a, b in zip(tr.iterations, tr.iterations[1:]))
+    if kind == "generic_warps4":
+        assert tr.meta["warps_in_flight"] == 4
