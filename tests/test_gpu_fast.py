@@ -298,7 +298,8 @@ def test_live_monitor_sees_every_epoch(cuda, kind):
     else:
         pen, part = pb.GroupL2Penalty(lam), pb.contiguous_partition(data.n_features, 10)
         cfg = pb.AsyncConfig(step_size="1/2L", epochs=epochs, seed=1, threads=2)
-    tr = pb.run_async(data, pb.Loss("logistic", lam), pen, part, cfg)
+    index = pb.build_support_index(data.features, part, drop_dead_blocks=True)
+    tr = pb.run_async(data, pb.Loss("logistic", lam), pen, part, cfg, index=index)
     assert len(tr.iterations) == epochs + 1, tr.iterations
     n = data.n_samples
     assert tr.iterations[0] == 0 and tr.iterations[-1] == epochs * n
