@@ -259,3 +259,32 @@ def test_bench_first_crossing_interpolation():
     # already under the target at the first checkpoint: interpolated from (0, rel 1)
     sec, ep = bench._first_crossing([50], [0.5], [1e-8], 100, 1e-6)
     assert 0 < sec < 0.5 and 0 < ep < 0.5
+
+
+def test_async_grid_launches_exactly_the_requested_warps():
+    """measure_speedup's c warps: ctas * warps_per_cta == c (c=12 ran 8 warps)."""
+    from types import SimpleNamespace
+
+    from paper_1707_06468_b200.asynchronous import _grid
+
+    for c in (1, 2, 3, 4, 8, 12, 20, 24, 32, 48, 100, 148, 4736):
+        ctas, wpc = _grid(None, SimpleNamespace(warps=c, warps_per_cta=0))
+        assert ctas * wpc == c, (c, ctas, wpc)
+        assert 1 <= wpc <= 32
+    assert _grid(None, SimpleNamespace(warps=None, warps_per_cta=0)) == (0, 0)
+    assert _grid(None, SimpleNamespace(warps=64, warps_per_cta=16)) == (4, 16)
+
+
+def test_bench_line_splits_long_numeric_arrays():
+    import importlib.util
+    from pathlib import Path
+
+    spec = importlib.util.spec_from_file_location("bench", Path(__file__).resolve().parents[1] / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    detail = {}
+    line = {"a": list(range(20)), "b": [1, 2], "c": [{"x": list(range(9)), "y": 1}], "d": {"e": [0.5] * 30}}
+    out = bench._split_arrays(line, "", detail)
+    assert out["b"] == [1, 2] and out["c"][0]["y"] == 1
+    assert set(detail) == {"a", "c[0].x", "d.e"}
+    assert detail["a"] == list(range(20)) and isinstance(out["a"], str)
