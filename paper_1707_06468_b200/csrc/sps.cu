@@ -1140,7 +1140,6 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
 
 }  // namespace ps
 #include "fast2.cuh"
-#include "fast3.cuh"
 namespace ps {
 
 // ---------------------------------------------------------------------------
@@ -1405,34 +1404,6 @@ template <typename VT, typename PT> static void *kernel_ptr_hot(int loss, int pe
     if (nc == 2)
         return literal ? kernel_ptr_hot_l<VT, PT, true, 2>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 2>(loss, pen);
     return literal ? kernel_ptr_hot_l<VT, PT, true, 1>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 1>(loss, pen);
-}
-template <typename VT, typename PT, bool LIT, int NC, int HM> static void *kernel_ptr_hot3_l(int loss, int pen)
-{
-    if (loss == PS_LOSS_LOGISTIC) {
-        if (pen == PS_PEN_L1) return (void *)sps_hot3_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, LIT, NC, HM>;
-        return (void *)sps_hot3_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, LIT, NC, HM>;
-    }
-    if (pen == PS_PEN_L1) return (void *)sps_hot3_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, LIT, NC, HM>;
-    return (void *)sps_hot3_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, LIT, NC, HM>;
-}
-template <typename VT, typename PT, int HM> static void *kernel_ptr_hot3_h(int loss, int pen, bool literal, int nc)
-{
-    if (nc == 2)
-        return literal ? kernel_ptr_hot3_l<VT, PT, true, 2, HM>(loss, pen) : kernel_ptr_hot3_l<VT, PT, false, 2, HM>(loss, pen);
-    return literal ? kernel_ptr_hot3_l<VT, PT, true, 1, HM>(loss, pen) : kernel_ptr_hot3_l<VT, PT, false, 1, HM>(loss, pen);
-}
-template <typename VT, typename PT> static void *kernel_ptr_hot3(int loss, int pen, bool literal, int nc, int hm)
-{
-    return hm > 512 ? kernel_ptr_hot3_h<VT, PT, 1024>(loss, pen, literal, nc) : kernel_ptr_hot3_h<VT, PT, 512>(loss, pen, literal, nc);
-}
-// third-generation hot kernel (fast3.cuh): staging capacity hm = 512 or 1024 slots
-static void *pick_hot3(const ps_csr_t *csr, int loss, int pen, bool literal, int nc, int hm)
-{
-    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (f64 && i64) return kernel_ptr_hot3<double, long long>(loss, pen, literal, nc, hm);
-    if (f64) return kernel_ptr_hot3<double, int>(loss, pen, literal, nc, hm);
-    if (i64) return kernel_ptr_hot3<float, long long>(loss, pen, literal, nc, hm);
-    return kernel_ptr_hot3<float, int>(loss, pen, literal, nc, hm);
 }
 static void *pick_hot(const ps_csr_t *csr, int loss, int pen, bool literal, int nc)
 {
@@ -1814,15 +1785,7 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         L->hot2 = L->fast && part->max_slots <= 64 && wpc == FAST_T / 32 && !(sched->flags & PS_FLAG_FAST_V1) &&
                   ((sched->flags >> 8) & 0xff) == 0 && !(sched->flags & PS_FLAG_ZERO_IMMEDIATE) &&
                   csr->n_rows < (int64_t(1) << 32);
-        if (L->hot2 && !(sched->flags & PS_FLAG_HOT_V2) && hot2_ncopy(sched->flags) == 1) {
-            // third generation (fast3.cuh): one pending copy, fixed staging offsets
-            const int hm = L->H > 512 ? 1024 : 512;
-            L->kernel = pick_hot3(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0,
-                                  part->max_slots <= 32 ? 1 : 2, hm);
-            L->ncopy = 1;
-            L->hot_doubles = (int)((hm > 512 ? Hot3<1024>::BYTES : Hot3<512>::BYTES) / 8);
-            L->smem = (size_t)L->hot_doubles * 8;
-        } else if (L->hot2) {
+        if (L->hot2) {
             L->kernel = pick_hot(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0,
                                  part->max_slots <= 32 ? 1 : 2);
             L->ncopy = hot2_ncopy(sched->flags);
