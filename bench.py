@@ -350,18 +350,17 @@ def lambda_path_bench(rank, world, epochs, ttt_epochs=30, with_oracle=True):
     B = 1
     while B < min(16, max(1, len(mine))):
         B *= 2
-    # the batched kernel pays from 8 lambdas per rank; below that the forks are
-    # faster per GPU
-    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", batched=B if B >= 8 else 0,
-                             concurrent=1 if B >= 8 else max(1, len(mine)))
+    # with the spread block layout the batched kernel is ahead of the forks at
+    # every share, 2 to 16 lambdas per rank
+    solve = lp.device_solver(d, loss, part, epochs=epochs, mode="async", batched=B)
     solve.batch([lams[k] for k in mine])  # warm-up
     reps_c = [timed(solve) for _ in range(3)]
     ms_c, obj_c, gap_c = sorted(reps_c, key=lambda r: r[0])[1]  # median of 3
-    dpb = solve.batched.dp if B >= 8 else solve.problem
+    dpb = solve.batched.dp
     s_ptr, s_val = (4 if dpb.row_ptr_type == 0 else 8), (4 if dpb.value_type == 0 else 8)
     kbar = dpb.nnz / dpb.n
     row_bytes = 2 * s_ptr + kbar * (4 + s_val) + s_val  # the CSR row + label, read once per B states
-    bpu_b = dpb.bytes_per_update() - ((1.0 - 1.0 / B) * row_bytes if B >= 8 else 0.0)
+    bpu_b = dpb.bytes_per_update() - (1.0 - 1.0 / B) * row_bytes
     out.update(ms=ms_c, ms_reps=[r[0] for r in reps_c], batched=B, bytes_per_update=bpu_b,
                bytes_per_update_unbatched=dpb.bytes_per_update(), mean_blocks_per_row=dpb.mean_blocks_per_row())
     del solve
@@ -867,8 +866,7 @@ def main():
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
                  "value": upd / (float(t[0].item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t[0].item()),
-                 "schedule": (f"lambda-batched kernel, B={lp_local['batched']} states per launch per rank"
-                              if lp_local["batched"] >= 8 else f"{lp_local['concurrent']} concurrent forks per rank"),
+                 "schedule": f"lambda-batched kernel, B={lp_local['batched']} states per launch per rank, spread block layout",
                  "concurrent_value": upd / (float(t[3].item()) / 1e3),
                  "concurrent_per_rank": lp_local["concurrent"], "rank0_ms_reps": lp_local["ms_reps"],
                  "rank0_certified_rel_gap_per_lambda_concurrent": lp_local["certified_rel_gap_concurrent"],

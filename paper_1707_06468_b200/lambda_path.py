@@ -211,18 +211,26 @@ class BatchedPath:
     step to all B states, so the sample, the CSR row and the per-row scalar
     work are shared.  State layout [block][q][beta](x, abar) on the device,
     alpha [n][beta]; the problem (CSR, partition, d_B) is the DeviceProblem's,
-    uploaded once (no hot-unit renumbering: blocks keep their ids)."""
+    uploaded once.
 
-    def __init__(self, data, loss, partition, B=16, device=None, dp=None):
+    ``spread`` (default): the DeviceProblem's hot-unit layout renumbers whole
+    blocks so that the most frequent ones sit 32 blocks apart (ps_hot_layout,
+    as for the staged kernels; nothing is staged here).  Every row commits to
+    the Zipf head's blocks; in the natural order those are adjacent and their
+    REDs queue in one L2 slice's atomic unit (ncu: 83% busy while the slice
+    average is 12%, profiles/ncu_sps_r02.md).  ``field`` returns original
+    coordinate order unless asked for the stored one."""
+
+    def __init__(self, data, loss, partition, B=16, device=None, dp=None, spread=True):
         from .device import DeviceProblem
         from .penalties import GroupL2Penalty
 
         if B not in (1, 2, 4, 8, 16):
             raise ValueError("B must be 1, 2, 4, 8 or 16")
         self.dp = dp if dp is not None else DeviceProblem(data, loss, GroupL2Penalty(0.0), partition, device=device,
-                                                          drop_dead_blocks=True, hot_max=0)
-        if self.dp.perm is not None:
-            raise ValueError("the batched path needs the natural block layout (hot_max=0)")
+                                                          drop_dead_blocks=True, hot_max=None if spread else 0)
+        if self.dp.perm is not None and self.dp.part_kind != "contiguous":
+            raise ValueError("the batched path needs a contiguous partition")
         torch = self.torch = self.dp.torch
         self.B = B
         dev = self.dp.device
@@ -233,6 +241,7 @@ class BatchedPath:
             self.lam2 = torch.zeros(B, dtype=torch.float64, device=dev)
             self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
             self.vec = torch.empty(self.dp.p_dev, dtype=torch.float64, device=dev)
+            self._perm_long = self.dp.perm.long() if self.dp.perm is not None else None
         self.slot_base = 0
 
     def reset(self, lams):
@@ -270,14 +279,18 @@ class BatchedPath:
             if samples is None:
                 self.slot_base += int(rows)
 
-    def field(self, beta, f=0):
-        """x (f=0) or abar (f=1) of state beta as a device p-vector."""
+    def field(self, beta, f=0, original=True):
+        """x (f=0) or abar (f=1) of state beta as a device vector: the p
+        coordinates in original order, or (original=False) the padded stored
+        order the device CSR uses."""
         from . import _lib
 
         with self.torch.cuda.device(self.dp.device):
             out = self.torch.empty(self.dp.p_dev, dtype=self.torch.float64, device=self.dp.device)
             _lib.check(_lib.load().ps_batch_field(self.state.data_ptr(), self.dp.p_dev, int(self.dp.part.G), self.B,
                                                   int(beta), int(f), out.data_ptr(), 0, _lib.stream_ptr()))
+            if original and self._perm_long is not None:
+                out = out[self._perm_long]
         return out
 
     def summary(self, beta, updates, keep_x=False):
@@ -285,7 +298,7 @@ class BatchedPath:
         from . import _lib
 
         dp = self.dp
-        x = self.field(beta)
+        x = self.field(beta, original=False)
         saved = dp.lam2
         dp.lam2 = float(self.lams[beta])
         with self.torch.cuda.device(dp.device):
@@ -296,7 +309,7 @@ class BatchedPath:
         out = {"objective": obj, "dual": dual, "gap": obj - dual, "nnz": int((x != 0).sum().item()),
                "norm": float(self.torch.linalg.vector_norm(x).item()), "updates": updates}
         if keep_x:
-            out["x"] = x.cpu().numpy()
+            out["x"] = (x[self._perm_long] if self._perm_long is not None else x).cpu().numpy()
         return out
 
 
