@@ -219,6 +219,17 @@ int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, 
  * in-flight row (sched->counter counts rows). */
 int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
                  int32_t B, double *state, double *alpha, const ps_sched_t *sched, void *stream);
+/* ps_batch_run with replicated x-delta accumulators for the hottest blocks of a
+ * spread hot-unit layout (ps_hot_layout; sched->hot_shift = its log2 stride):
+ * in asynchronous mode the nrb most frequent stored units (unit r << hot_shift,
+ * r < nrb) commit their x deltas to one of nrep replicas (chosen by warp), so a
+ * hot block's REDs queue on nrep L2 lines instead of one; reads sum the state
+ * and the replicas, and the replicas are folded into the state after the
+ * launch (same stream).  xrep: device, nrep*nrb*G*B doubles, zero on entry and
+ * left zero.  nrep = 0 or xrep = NULL: ps_batch_run. */
+int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
+                     int32_t B, double *state, double *alpha, const ps_sched_t *sched, double *xrep, int32_t nrep,
+                     int32_t nrb, void *stream);
 /* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state) */
 int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
                    int32_t set, void *stream);

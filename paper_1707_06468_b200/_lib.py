@@ -37,7 +37,7 @@ EXPORTS = (
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels", "ps_timestamp",
     "ps_dual_objective", "ps_run_monitored", "ps_libsvm_index", "ps_libsvm_scan", "ps_libsvm_fill",
-    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv", "ps_loss_eval", "ps_batch_run", "ps_batch_field",
+    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv", "ps_loss_eval", "ps_batch_run", "ps_batch_run_rep", "ps_batch_field",
 )
 
 _vp = ctypes.c_void_p
@@ -114,6 +114,7 @@ def load():
         "ps_loss_deriv": (_i32, [_i32, _i32, _vp, _vp, _i64, _vp, _vp]),
         "ps_loss_eval": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp]),
         "ps_batch_run": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _i32, _vp, _vp, _P(Sched), _vp]),
+        "ps_batch_run_rep": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _i32, _vp, _vp, _P(Sched), _vp, _i32, _i32, _vp]),
         "ps_batch_field": (_i32, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp]),
         "ps_libsvm_scan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ps_libsvm_fill": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -46,6 +46,12 @@ struct BArgs {
     uint64_t seed, slot_base;
     unsigned long long *counter;
     int32_t det, skip_zero;
+    // replicated x-delta accumulators of the hottest blocks (asynchronous mode):
+    // stored block b with (b & hmask) == 0 and rank b >> hshift < nrb commits its
+    // x deltas to replica (warp % nrep) of xrep[nrep][nrb][G][B]; a read of its x
+    // is the state's x plus every replica; k_batch_fold folds them after the launch
+    double *xrep;
+    int32_t nrep, nrb, hshift;
 };
 
 constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
@@ -68,7 +74,19 @@ __host__ __device__ __forceinline__ int64_t bidx(int64_t j, int beta, int64_t nb
     return (((int64_t)(beta / S) * nb * G + j) * S + beta % S) * 2;
 }
 
-template <typename VT, int LOSS, int B, int GT>
+// rank of a replicated hot block, or -1
+template <bool REP> __device__ __forceinline__ int rep_rank(const BArgs &a, int64_t b)
+{
+    if (!REP) return -1;
+    const int64_t r = b >> a.hshift;
+    return ((b & ((1ll << a.hshift) - 1)) == 0 && r < a.nrb) ? (int)r : -1;
+}
+__device__ __forceinline__ double *rep_ptr(const BArgs &a, int rr, int rank, int q, int beta, int B, int G)
+{
+    return a.xrep + (((int64_t)rr * a.nrb + rank) * G + q) * B + beta;
+}
+
+template <typename VT, int LOSS, int B, int GT, bool REP>
 __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
 {
     constexpr int LPB = 32 / B;                                  // lanes per state
@@ -121,6 +139,9 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
             const int e = sub + LPB * j;
             const int ce = __shfl_sync(FULL, col, e & 31);
             xm[j] = (e < k) ? ld_cg(st + bidx(ce, beta, a.nb, G, S)) : 0.0;
+            const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
+            if (rk >= 0)
+                for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
         }
         const int blk = col >= 0 ? col / G : -1 - lane;
         const unsigned peers = __match_any_sync(FULL, blk);
@@ -163,10 +184,13 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
         auto load_blk = [&](int tb, double2 *v) {
             const int b = sblk[tb];
             const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
+            const int rk = rep_rank<REP>(a, b);
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
                 v[r] = q < nq ? ld_cg2(st + bidx((int64_t)b * G + q, beta, a.nb, G, S)) : make_double2(0.0, 0.0);
+                if (rk >= 0 && q < nq)
+                    for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
         };
         if (g > 0) load_blk(0, cur);
@@ -201,15 +225,22 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
             // zero block kept at zero: delta 0, nothing committed (the lane
             // kernel's skip); a zeroed block is stored (zero commits)
             if (!(f == 0.0 && zero && a.skip_zero)) {
+                const int rk = a.det ? -1 : rep_rank<REP>(a, b);
 #pragma unroll
                 for (int r = 0; r < RMAX; r++) {
                     const int q = sub + LPB * r;
                     if (q < nq) {
                         double *px = st + bidx((int64_t)b * G + q, beta, a.nb, G, S);
                         const double z = u[r] * f;
-                        if (a.det) *px = cur[r].x + (z - cur[r].x);
-                        else if (f == 0.0) atomic_exch(px, 0.0);
-                        else red_add(px, z - cur[r].x);
+                        if (a.det) {
+                            *px = cur[r].x + (z - cur[r].x);
+                        } else if (f == 0.0) {  // a zeroed block is stored: the state and every replica
+                            atomic_exch(px, 0.0);
+                            if (rk >= 0)
+                                for (int rr = 0; rr < a.nrep; rr++) atomic_exch(rep_ptr(a, rr, rk, q, beta, B, G), 0.0);
+                        } else {
+                            red_add(rk >= 0 ? rep_ptr(a, (int)(gw % a.nrep), rk, q, beta, B, G) : px, z - cur[r].x);
+                        }
                     }
                 }
             }
@@ -239,20 +270,24 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
     if (!a.det && lane == 0 && done % PROGRESS_BATCH_B) atomicAdd(a.counter, (unsigned long long)(done % PROGRESS_BATCH_B));
 }
 
-template <typename VT, int LOSS, int GT> static void *pick_bg(int B)
+template <typename VT, int LOSS, int GT, bool REP> static void *pick_bgr(int B)
 {
     switch (B) {
-    case 1: return (void *)sps_group_batch_kernel<VT, LOSS, 1, GT>;
-    case 2: return (void *)sps_group_batch_kernel<VT, LOSS, 2, GT>;
-    case 4: return (void *)sps_group_batch_kernel<VT, LOSS, 4, GT>;
-    case 8: return (void *)sps_group_batch_kernel<VT, LOSS, 8, GT>;
-    default: return (void *)sps_group_batch_kernel<VT, LOSS, 16, GT>;
+    case 1: return (void *)sps_group_batch_kernel<VT, LOSS, 1, GT, REP>;
+    case 2: return (void *)sps_group_batch_kernel<VT, LOSS, 2, GT, REP>;
+    case 4: return (void *)sps_group_batch_kernel<VT, LOSS, 4, GT, REP>;
+    case 8: return (void *)sps_group_batch_kernel<VT, LOSS, 8, GT, REP>;
+    default: return (void *)sps_group_batch_kernel<VT, LOSS, 16, GT, REP>;
     }
 }
-// G = 10 (BASELINE config 5) specialised, other G <= 16 at runtime
-template <typename VT, int LOSS> static void *pick_b(int B, int G)
+template <typename VT, int LOSS, int GT> static void *pick_bg(int B, bool rep)
 {
-    return G == 10 ? pick_bg<VT, LOSS, 10>(B) : pick_bg<VT, LOSS, 0>(B);
+    return rep ? pick_bgr<VT, LOSS, GT, true>(B) : pick_bgr<VT, LOSS, GT, false>(B);
+}
+// G = 10 (BASELINE config 5) specialised, other G <= 16 at runtime
+template <typename VT, int LOSS> static void *pick_b(int B, int G, bool rep)
+{
+    return G == 10 ? pick_bg<VT, LOSS, 10>(B, rep) : pick_bg<VT, LOSS, 0>(B, rep);
 }
 
 __global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G, int B, int beta, int field,
@@ -266,12 +301,34 @@ __global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G,
     }
 }
 
+// fold the replicated x deltas of the hot blocks into the state (after a launch)
+__global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int hshift, int64_t nb, int G, int B,
+                             int64_t p)
+{
+    const int S = B < BATCH_S ? B : BATCH_S;
+    const int64_t m = (int64_t)nrb * G * B;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int beta = (int)(t % B);
+        const int64_t rq = t / B;
+        const int q = (int)(rq % G), rank = (int)(rq / G);
+        double sum = 0.0;
+        for (int rr = 0; rr < nrep; rr++) {
+            double *r = xrep + (int64_t)rr * m + t;
+            sum += *r;
+            *r = 0.0;
+        }
+        const int64_t j = ((int64_t)rank << hshift) * G + q;
+        if (j < p) state[bidx(j, beta, nb, G, S)] += sum;
+    }
+}
+
 }  // namespace ps
 
 using namespace ps;
 
-extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
-                            int32_t B, double *state, double *alpha, const ps_sched_t *sched, void *stream)
+extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
+                                const double *lam2, int32_t B, double *state, double *alpha, const ps_sched_t *sched,
+                                double *xrep, int32_t nrep, int32_t nrb, void *stream)
 {
     NvtxRange nvtx_range("K2b ps_batch_run");
     if (!csr || !part || !prm || !lam2 || !state || !alpha || !sched) return ps_fail(PS_EINVAL, "null argument");
@@ -315,11 +372,16 @@ extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps
     a.counter = sched->counter;
     a.det = det ? 1 : 0;
     a.skip_zero = (sched->flags & PS_FLAG_GROUP_STORE_ZEROS) ? 0 : 1;
+    a.xrep = xrep;
+    a.nrep = (!det && xrep && nrep > 0 && nrb > 0) ? nrep : 0;
+    a.nrb = nrb;
+    a.hshift = std::max(0, (int)sched->hot_shift);
     void *kern;
     const bool f64 = csr->value_type == PS_F64, sq = prm->loss == PS_LOSS_SQUARED;
     const int G = part->G;
-    if (f64) kern = sq ? pick_b<double, PS_LOSS_SQUARED>(B, G) : pick_b<double, PS_LOSS_LOGISTIC>(B, G);
-    else kern = sq ? pick_b<float, PS_LOSS_SQUARED>(B, G) : pick_b<float, PS_LOSS_LOGISTIC>(B, G);
+    const bool rep = a.nrep > 0;
+    if (f64) kern = sq ? pick_b<double, PS_LOSS_SQUARED>(B, G, rep) : pick_b<double, PS_LOSS_LOGISTIC>(B, G, rep);
+    else kern = sq ? pick_b<float, PS_LOSS_SQUARED>(B, G, rep) : pick_b<float, PS_LOSS_LOGISTIC>(B, G, rep);
     const int wpc = sched->warps_per_cta > 0 ? std::min(sched->warps_per_cta, BATCH_T / 32) : BATCH_T / 32;
     const size_t smem = (size_t)wpc * BATCH_SM_WARP * 8;
     if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -337,7 +399,19 @@ extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps
     a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
     void *args[] = {(void *)&a};
     CK(cudaLaunchKernel(kern, dim3(ctas), dim3(wpc * 32), args, smem, (cudaStream_t)stream), "ps_batch_run launch");
+    if (a.nrep > 0) {
+        const int64_t m = (int64_t)nrb * G * B;
+        k_batch_fold<<<(int)std::min<int64_t>((m + 255) / 256, 1024), 256, 0, (cudaStream_t)stream>>>(
+            state, xrep, a.nrep, nrb, a.hshift, a.nb, G, B, a.p);
+        CK(cudaGetLastError(), "ps_batch_run fold");
+    }
     return PS_OK;
+}
+
+extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
+                            int32_t B, double *state, double *alpha, const ps_sched_t *sched, void *stream)
+{
+    return ps_batch_run_rep(csr, part, prm, lam2, B, state, alpha, sched, nullptr, 0, 0, stream);
 }
 
 extern "C" int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,

@@ -219,9 +219,21 @@ class BatchedPath:
     the Zipf head's blocks; in the natural order those are adjacent and their
     REDs queue in one L2 slice's atomic unit (ncu: 83% busy while the slice
     average is 12%, profiles/ncu_sps_r02.md).  ``field`` returns original
-    coordinate order unless asked for the stored one."""
+    coordinate order unless asked for the stored one.
 
-    def __init__(self, data, loss, partition, B=16, device=None, dp=None, spread=True):
+    ``nrep`` > 0 (default by B, AUTO_NREP): the x deltas of the ``nrb`` hottest
+    blocks go to nrep replica accumulators (one per warp residue), folded into
+    the state after each launch (ps_batch_run_rep).  With few states per row a
+    hot block's x lines receive a RED from every row, and the per-line atomic
+    rate caps the solve (~48 M rows/s at B = 2 whatever the grid)."""
+
+    # replicas (and replicated hottest blocks) of the x-delta accumulators by B
+    # (config 5, tools/gpu/exp_batch_rep.py: B = 2 / 4 / 8 +56% / +70% / +16%
+    # rows/s; at B = 16 the extra replica loads cost more than the spread REDs save)
+    AUTO_NREP = {1: 8, 2: 8, 4: 8, 8: 4, 16: 0}
+    AUTO_NRB = {1: 32, 2: 32, 4: 64, 8: 16, 16: 0}
+
+    def __init__(self, data, loss, partition, B=16, device=None, dp=None, spread=True, nrep=None, nrb=None):
         from .device import DeviceProblem
         from .penalties import GroupL2Penalty
 
@@ -242,6 +254,15 @@ class BatchedPath:
             self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
             self.vec = torch.empty(self.dp.p_dev, dtype=torch.float64, device=dev)
             self._perm_long = self.dp.perm.long() if self.dp.perm is not None else None
+            # replicated x-delta accumulators of the nrb hottest blocks (ps_batch_run_rep;
+            # needs the spread layout, whose hot units are the blocks r << hot_shift)
+            units = self.dp.H // G if self.dp.perm is not None else 0
+            nrep = self.AUTO_NREP[B] if nrep is None else nrep
+            nrb = self.AUTO_NRB[B] if nrb is None else nrb
+            self.nrb = min(int(nrb), units) if nrep > 0 else 0
+            self.nrep = int(nrep) if self.nrb > 0 else 0
+            self.xrep = (torch.zeros(max(1, self.nrep * self.nrb * G * B), dtype=torch.float64, device=dev)
+                         if self.nrep else None)
         self.slot_base = 0
 
     def reset(self, lams):
@@ -272,10 +293,12 @@ class BatchedPath:
             else:
                 self.counter.zero_()
             sched = _lib.Sched(ptr, int(rows), int(seed) & (2 ** 64 - 1), int(self.slot_base), self.counter.data_ptr(),
-                               0, int(ctas), int(warps_per_cta), 0, float(contention), 0, 0, 0, 0, None, None)
-            _lib.check(_lib.load().ps_batch_run(dp.csr, dp.part, dp.params(gamma), self.lam2.data_ptr(), self.B,
-                                                self.state.data_ptr(), self.alpha.data_ptr(), sched,
-                                                _lib.stream_ptr(stream)))
+                               0, int(ctas), int(warps_per_cta), 0, float(contention), 0, 0, int(dp.hot_shift), 0, None,
+                               None)
+            _lib.check(_lib.load().ps_batch_run_rep(dp.csr, dp.part, dp.params(gamma), self.lam2.data_ptr(), self.B,
+                                                    self.state.data_ptr(), self.alpha.data_ptr(), sched,
+                                                    self.xrep.data_ptr() if self.nrep else None, self.nrep, self.nrb,
+                                                    _lib.stream_ptr(stream)))
             if samples is None:
                 self.slot_base += int(rows)
 

@@ -50,17 +50,23 @@ def test_batched_deterministic_replay_matches_single_lambda(cuda, B, small_cases
             assert _rel(x, g["grp_contig__x"][0]) <= 1e-9
 
 
-def test_batched_async_reaches_each_optimum(cuda):
+@pytest.mark.parametrize("B,factors", [(8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005)), (2, (0.3, 0.01))],
+                         ids=["B8", "B2"])
+def test_batched_async_reaches_each_optimum(cuda, B, factors):
+    """Spread block layout; the hottest blocks commit their x deltas
+    through replicated accumulators (ps_batch_run_rep, folded after the launch)."""
     rng = np.random.default_rng(11)
     data = problems._zipf_logistic(rng, 8000, 40000, 20, 1.1, 100)
     part = pb.contiguous_partition(data.n_features, 10)
     lam1 = 1.0 / data.n_samples
     loss = pb.Loss("logistic", lam1)
     lmax = pb.group_lambda_max(data, part)
-    lams = [f * lmax for f in (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005)]
-    solve = device_solver(data, loss, part, epochs=60, seed=3, batched=8)
+    lams = [f * lmax for f in factors]
+    solve = device_solver(data, loss, part, epochs=60, seed=3, batched=B)
     res = solve.batch(lams)
     bp = solve.batched
+    assert bp.dp.perm is not None  # spread layout
+    assert bp.nrep == BatchedPath.AUTO_NREP[B] > 0  # replicated hottest blocks at both B
     n = data.n_samples
     for beta, (lam, r) in enumerate(zip(lams, res)):
         dp = DeviceProblem(data, loss, pb.GroupL2Penalty(lam), part, drop_dead_blocks=True, hot_max=0)
@@ -70,6 +76,6 @@ def test_batched_async_reaches_each_optimum(cuda):
         assert abs(r["objective"] - fref) <= 1e-6 * abs(fref), (lam / lmax, r["objective"], fref)
         assert r["gap"] >= -1e-12 and r["objective"] >= r["dual"]
         # abar stays the exact average of this state's alpha table
-        dp.alpha.copy_(bp.alpha.view(-1, 8)[:, beta])
+        dp.alpha.copy_(bp.alpha.view(-1, B)[:, beta])
         dp.resync_average()
         assert np.max(np.abs(bp.field(beta, 1).cpu().numpy() - dp.abar())) <= 1e-12

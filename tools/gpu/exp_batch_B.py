@@ -14,7 +14,8 @@ lams = lp.lambda_grid(pb.group_lambda_max(d, part), 16, 1e-3)
 for world in (1, 2, 4, 8):
     mine = [lams[k] for k in lp.assign(lams, world)[0]]
     B = len(mine)
-    for kw, tag in ((dict(batched=B), "batched"), (dict(concurrent=B), "concurrent")):
+    modes = ((dict(batched=B), "batched"),) + (((dict(concurrent=B), "concurrent"),) if "--forks" in sys.argv else ())
+    for kw, tag in modes:
         s = lp.device_solver(d, loss, part, epochs=E, mode="async", **kw)
         s.batch(mine); torch.cuda.synchronize()
         ts = []
