@@ -210,9 +210,9 @@ int ps_loss_deriv(int32_t loss, int32_t fast, const double *z, const double *b, 
  * B in {1,2,4,8,16} solves of the same problem that differ only in the group
  * weight lam2[beta] (device, B doubles; prm->lam2 is ignored), sharing each
  * sampled row: saga.py:150-185 / asynchronous.py:80-117 per state.  State:
- * NB*G*B*2 doubles (NB = ceil(p/G)), coordinate j of state beta at
- * (((beta/S)*NB*G + j)*S + beta%S)*2 + {0: x, 1: abar} with S = min(B, 2)
- * (use ps_batch_field); alpha[i*B + beta]; d_B from ps_prepare (part->blk_weight).
+ * ps_batch_state_doubles(p, G, B) doubles (NB = ceil(p/G)), coordinate j of
+ * state beta at (beta/S)*RPAD + (((beta/S)*NB*G + j)*S + beta%S)*2 + {0: x, 1: abar}
+ * with S = min(B, 2) and RPAD the region pad (use ps_batch_field); alpha[i*B + beta]; d_B from ps_prepare (part->blk_weight).
  * CONTIG partitions of G <= 16, rows <= 32 nonzeros, int32 row pointers.
  * sched->samples != NULL: deterministic replay of the sequence on one warp
  * (every state takes the same samples); else asynchronous, one warp per
@@ -230,6 +230,14 @@ int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *
 int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, const double *lam2,
                      int32_t B, double *state, double *alpha, const ps_sched_t *sched, double *xrep, int32_t nrep,
                      int32_t nrb, void *stream);
+/* doubles of a ps_batch_run state for p coordinates, blocks of G, B states
+ * (regions of two states, each followed by the current region pad), and of the
+ * replica accumulators of ps_batch_run_rep */
+int64_t ps_batch_state_doubles(int64_t p, int32_t G, int32_t B);
+int64_t ps_batch_rep_doubles(int32_t nrep, int32_t nrb, int32_t G, int32_t B);
+/* diagnostics: the state's region pad and the replica chunk stride, in doubles
+ * (process-wide; allocate states after setting them) */
+int ps_batch_tune(int64_t rpad, int64_t rstride);
 /* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state) */
 int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
                    int32_t set, void *stream);

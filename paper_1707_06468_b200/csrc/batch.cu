@@ -52,6 +52,7 @@ struct BArgs {
     // is the state's x plus every replica; k_batch_fold folds them after the launch
     double *xrep;
     int32_t nrep, nrb, hshift;
+    int64_t rpad, rstride;  // state region pad; doubles per (replica, hot block) chunk
 };
 
 constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
@@ -69,10 +70,15 @@ constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
 constexpr int BATCH_S = 2;
 constexpr int PROGRESS_BATCH_B = 16;           // rows per progress bump of a warp
 constexpr int BATCH_SM_WARP = 32 + 32 * 16;    // per-warp shared doubles: block ids + row values [32][16]
-__host__ __device__ __forceinline__ int64_t bidx(int64_t j, int beta, int64_t nb, int G, int S)
+// region g of the state starts at g * (nb*G*S*2 + rpad) doubles: the pad keeps
+// the regions' copies of a hot block from aliasing onto the same L2 slice
+__host__ __device__ __forceinline__ int64_t bidx(int64_t j, int beta, int64_t nb, int G, int S, int64_t rpad)
 {
-    return (((int64_t)(beta / S) * nb * G + j) * S + beta % S) * 2;
+    return (int64_t)(beta / S) * rpad + (((int64_t)(beta / S) * nb * G + j) * S + beta % S) * 2;
 }
+// layout knobs (doubles): the region pad and the stride of one (replica, hot
+// block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
+static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
 
 // rank of a replicated hot block, or -1
 template <bool REP> __device__ __forceinline__ int rep_rank(const BArgs &a, int64_t b)
@@ -83,7 +89,7 @@ template <bool REP> __device__ __forceinline__ int rep_rank(const BArgs &a, int6
 }
 __device__ __forceinline__ double *rep_ptr(const BArgs &a, int rr, int rank, int q, int beta, int B, int G)
 {
-    return a.xrep + (((int64_t)rr * a.nrb + rank) * G + q) * B + beta;
+    return a.xrep + ((int64_t)rr * a.nrb + rank) * a.rstride + q * B + beta;
 }
 
 template <typename VT, int LOSS, int B, int GT, bool REP>
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
         for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
             const int e = sub + LPB * j;
             const int ce = __shfl_sync(FULL, col, e & 31);
-            xm[j] = (e < k) ? ld_cg(st + bidx(ce, beta, a.nb, G, S)) : 0.0;
+            xm[j] = (e < k) ? ld_cg(st + bidx(ce, beta, a.nb, G, S, a.rpad)) : 0.0;
             const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
             if (rk >= 0)
                 for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
-                v[r] = q < nq ? ld_cg2(st + bidx((int64_t)b * G + q, beta, a.nb, G, S)) : make_double2(0.0, 0.0);
+                v[r] = q < nq ? ld_cg2(st + bidx((int64_t)b * G + q, beta, a.nb, G, S, a.rpad)) : make_double2(0.0, 0.0);
                 if (rk >= 0 && q < nq)
                     for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
                 for (int r = 0; r < RMAX; r++) {
                     const int q = sub + LPB * r;
                     if (q < nq) {
-                        double *px = st + bidx((int64_t)b * G + q, beta, a.nb, G, S);
+                        double *px = st + bidx((int64_t)b * G + q, beta, a.nb, G, S, a.rpad);
                         const double z = u[r] * f;
                         if (a.det) {
                             *px = cur[r].x + (z - cur[r].x);
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
             const int ce = __shfl_sync(FULL, col, e & 31);
             const double ve = __shfl_sync(FULL, val, e & 31);
             if (e < k) {
-                double *pab = st + bidx(ce, beta, a.nb, G, S) + 1;
+                double *pab = st + bidx(ce, beta, a.nb, G, S, a.rpad) + 1;
                 if (a.det) *pab = *pab + tq * ve;
                 else red_add(pab, tq * ve);
             }
@@ -291,11 +297,11 @@ template <typename VT, int LOSS> static void *pick_b(int B, int G, bool rep)
 }
 
 __global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G, int B, int beta, int field,
-                              double *out, int set)
+                              double *out, int set, int64_t rpad)
 {
     const int S = B < BATCH_S ? B : BATCH_S;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
-        double *s = const_cast<double *>(state) + bidx(j, beta, nb, G, S) + field;
+        double *s = const_cast<double *>(state) + bidx(j, beta, nb, G, S, rpad) + field;
         if (set) *s = out[j];
         else out[j] = *s;
     }
@@ -303,7 +309,7 @@ __global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G,
 
 // fold the replicated x deltas of the hot blocks into the state (after a launch)
 __global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int hshift, int64_t nb, int G, int B,
-                             int64_t p)
+                             int64_t p, int64_t rpad, int64_t rstride)
 {
     const int S = B < BATCH_S ? B : BATCH_S;
     const int64_t m = (int64_t)nrb * G * B;
@@ -313,12 +319,12 @@ __global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int
         const int q = (int)(rq % G), rank = (int)(rq / G);
         double sum = 0.0;
         for (int rr = 0; rr < nrep; rr++) {
-            double *r = xrep + (int64_t)rr * m + t;
+            double *r = xrep + ((int64_t)rr * nrb + rank) * rstride + q * B + beta;
             sum += *r;
             *r = 0.0;
         }
         const int64_t j = ((int64_t)rank << hshift) * G + q;
-        if (j < p) state[bidx(j, beta, nb, G, S)] += sum;
+        if (j < p) state[bidx(j, beta, nb, G, S, rpad)] += sum;
     }
 }
 
@@ -376,6 +382,8 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     a.nrep = (!det && xrep && nrep > 0 && nrb > 0) ? nrep : 0;
     a.nrb = nrb;
     a.hshift = std::max(0, (int)sched->hot_shift);
+    a.rpad = g_rpad;
+    a.rstride = std::max<int64_t>(g_rstride, (int64_t)part->G * B);
     void *kern;
     const bool f64 = csr->value_type == PS_F64, sq = prm->loss == PS_LOSS_SQUARED;
     const int G = part->G;
@@ -402,7 +410,7 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     if (a.nrep > 0) {
         const int64_t m = (int64_t)nrb * G * B;
         k_batch_fold<<<(int)std::min<int64_t>((m + 255) / 256, 1024), 256, 0, (cudaStream_t)stream>>>(
-            state, xrep, a.nrep, nrb, a.hshift, a.nb, G, B, a.p);
+            state, xrep, a.nrep, nrb, a.hshift, a.nb, G, B, a.p, a.rpad, a.rstride);
         CK(cudaGetLastError(), "ps_batch_run fold");
     }
     return PS_OK;
@@ -421,7 +429,29 @@ extern "C" int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, in
     if (p <= 0) return PS_OK;
     const int64_t nb = (p + G - 1) / G;
     k_batch_field<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(state, p, nb, G, B,
-                                                                                                  beta, field, vec, set);
+                                                                                                  beta, field, vec, set, g_rpad);
     CK(cudaGetLastError(), "ps_batch_field launch");
     return PS_OK;
+}
+
+extern "C" int ps_batch_tune(int64_t rpad, int64_t rstride)
+{
+    if (rpad < 0 || rstride < 0) return ps_fail(PS_EINVAL, "bad argument");
+    g_rpad = rpad;
+    g_rstride = rstride;
+    return PS_OK;
+}
+
+extern "C" int64_t ps_batch_state_doubles(int64_t p, int32_t G, int32_t B)
+{
+    if (p < 0 || G < 1 || B < 1) return -1;
+    const int S = B < BATCH_S ? B : BATCH_S;
+    const int64_t nb = (p + G - 1) / G;
+    return (int64_t)(B / S) * (nb * G * S * 2 + g_rpad);
+}
+
+extern "C" int64_t ps_batch_rep_doubles(int32_t nrep, int32_t nrb, int32_t G, int32_t B)
+{
+    if (nrep < 0 || nrb < 0 || G < 1 || B < 1) return -1;
+    return (int64_t)nrep * nrb * std::max<int64_t>(g_rstride, (int64_t)G * B);
 }

@@ -234,6 +234,7 @@ class BatchedPath:
     AUTO_NRB = {1: 32, 2: 32, 4: 64, 8: 16, 16: 0}
 
     def __init__(self, data, loss, partition, B=16, device=None, dp=None, spread=True, nrep=None, nrb=None):
+        from . import _lib
         from .device import DeviceProblem
         from .penalties import GroupL2Penalty
 
@@ -248,7 +249,8 @@ class BatchedPath:
         dev = self.dp.device
         with torch.cuda.device(dev):
             G = int(self.dp.part.G)
-            self.state = torch.zeros(-(-self.dp.p_dev // G) * G * B * 2, dtype=torch.float64, device=dev)
+            self.state = torch.zeros(int(_lib.load().ps_batch_state_doubles(self.dp.p_dev, G, B)), dtype=torch.float64,
+                                     device=dev)
             self.alpha = torch.zeros(self.dp.n * B, dtype=torch.float64, device=dev)
             self.lam2 = torch.zeros(B, dtype=torch.float64, device=dev)
             self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -261,8 +263,8 @@ class BatchedPath:
             nrb = self.AUTO_NRB[B] if nrb is None else nrb
             self.nrb = min(int(nrb), units) if nrep > 0 else 0
             self.nrep = int(nrep) if self.nrb > 0 else 0
-            self.xrep = (torch.zeros(max(1, self.nrep * self.nrb * G * B), dtype=torch.float64, device=dev)
-                         if self.nrep else None)
+            self.xrep = (torch.zeros(int(_lib.load().ps_batch_rep_doubles(self.nrep, self.nrb, G, B)),
+                                     dtype=torch.float64, device=dev) if self.nrep else None)
         self.slot_base = 0
 
     def reset(self, lams):
