@@ -384,6 +384,25 @@ def lambda_path_bench(rank, world, epochs, ttt_epochs=30, with_oracle=True):
     ms_s, obj_s, gap_s = sorted(reps_s, key=lambda r: r[0])[1]
     del serial
     torch.cuda.empty_cache()
+    if world == 1:
+        # what each rank of an N-GPU run would time, measured here: rank 0's
+        # longest-work-first share of the 16 lambdas at N = 2 / 4 / 8, one
+        # lambda-batched launch (B = 16 / N) as the N-GPU path runs it
+        shares = []
+        for w in (2, 4, 8):
+            mine_w = lp.assign(lams, w)[0]
+            sw = lp.device_solver(d, loss, part, epochs=epochs, mode="async", batched=len(mine_w))
+            sw.batch([lams[k] for k in mine_w])  # warm-up
+            mine = mine_w
+            reps_w = [timed(sw) for _ in range(3)]
+            ms_w = sorted(r[0] for r in reps_w)[1]
+            shares.append({"n_gpus": w, "lambdas_per_rank": len(mine_w), "rank0_ms": ms_w,
+                           "per_gpu_value": len(mine_w) * epochs * n / (ms_w / 1e3),
+                           "path_value_if_ranks_equal": 16 * epochs * n / (ms_w / 1e3)})
+            del sw
+            torch.cuda.empty_cache()
+        mine = lp.assign(lams, world)[rank]
+        out["rank_shares"] = shares
     if ttt_epochs > 0:
         out["per_lambda"] = lambda_path_ttt(cfg, lams, mine, ttt_epochs, with_oracle=with_oracle)
     out.update(ms_serial=ms_s, ms_serial_reps=[r[0] for r in reps_s],
@@ -879,6 +898,10 @@ def main():
                  "mean_blocks_per_row": lp_local["mean_blocks_per_row"],
                  "roofline_frac_per_gpu": upd / (float(t[0].item()) / 1e3) / world * lp_local["bytes_per_update"]
                  / 1e9 / peak}
+        if "rank_shares" in lp_local:
+            lpath["rank_shares_measured_on_this_gpu"] = lp_local["rank_shares"]
+            lpath["rank_shares_note"] = ("one GPU, rank 0's share of an N-GPU run timed alone (the N-GPU path has "
+                                         "no collective in the solve; its time is the max over ranks)")
         if "per_lambda" in lp_local:
             per = lp_local["per_lambda"]
             if dist:

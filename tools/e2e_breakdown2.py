@@ -21,7 +21,7 @@ def wrap(obj, name):
         torch.cuda.synchronize(); t = time.perf_counter(); r = fn(*a, **k); torch.cuda.synchronize()
         T[name] = T.get(name, 0.0) + (time.perf_counter() - t) * 1e3; return r
     setattr(obj, name, w)
-for nm in ("_hot_layout", "_setup_partition", "run_async_checkpointed", "objective", "objective_parts", "x", "reset_state"):
+for nm in ("__init__", "_hot_layout", "_setup_partition", "run_async_monitored", "run_async_checkpointed", "objective", "objective_parts", "x", "reset_state", "launch_config"):
     wrap(device.DeviceProblem, nm)
 for rep in range(4):
     T.clear()
