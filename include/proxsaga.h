@@ -141,8 +141,6 @@ typedef struct ps_sched {
                                             zero delta is skipped; diagnostics) */
 #define PS_FLAG_FAST_V1 4194304   /* singleton fast path: the round-1 kernel (sps_fast_kernel: dirty bitmasks,
                                       two pending copies) instead of sps_hot_kernel (A/B, diagnostics) */
-#define PS_FLAG_LANE 8388608      /* singleton rows of <= 32 nonzeros: one thread per in-flight sample
-                                      (sps_lane_kernel, lane.cuh; warps_per_cta warps per CTA, default 4) */
 #define PS_FLAG_NO_CLUSTER 2097152 /* fast kernel: no CTA pairs (each CTA refreshes its hot snapshot
                                       from L2; default: clusters of 2 share one refresh) */
 

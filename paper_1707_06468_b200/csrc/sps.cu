@@ -1140,7 +1140,6 @@ __global__ void __launch_bounds__(MAXT, 1) sps_fast_kernel(const KArgs a)
 
 }  // namespace ps
 #include "fast2.cuh"
-#include "lane.cuh"
 namespace ps {
 
 // ---------------------------------------------------------------------------
@@ -1405,30 +1404,6 @@ template <typename VT, typename PT> static void *kernel_ptr_hot(int loss, int pe
     if (nc == 2)
         return literal ? kernel_ptr_hot_l<VT, PT, true, 2>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 2>(loss, pen);
     return literal ? kernel_ptr_hot_l<VT, PT, true, 1>(loss, pen) : kernel_ptr_hot_l<VT, PT, false, 1>(loss, pen);
-}
-template <typename VT, typename PT, bool LIT, int KM> static void *kernel_ptr_lane_l(int loss, int pen)
-{
-    if (loss == PS_LOSS_LOGISTIC) {
-        if (pen == PS_PEN_L1) return (void *)sps_lane_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_L1, LIT, KM>;
-        return (void *)sps_lane_kernel<VT, PT, PS_LOSS_LOGISTIC, PS_PEN_ZERO, LIT, KM>;
-    }
-    if (pen == PS_PEN_L1) return (void *)sps_lane_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_L1, LIT, KM>;
-    return (void *)sps_lane_kernel<VT, PT, PS_LOSS_SQUARED, PS_PEN_ZERO, LIT, KM>;
-}
-template <typename VT, typename PT> static void *kernel_ptr_lane(int loss, int pen, bool literal, int km)
-{
-    if (km > 24)
-        return literal ? kernel_ptr_lane_l<VT, PT, true, 32>(loss, pen) : kernel_ptr_lane_l<VT, PT, false, 32>(loss, pen);
-    return literal ? kernel_ptr_lane_l<VT, PT, true, 24>(loss, pen) : kernel_ptr_lane_l<VT, PT, false, 24>(loss, pen);
-}
-// thread-per-sample kernel (lane.cuh): rows of <= 24 or <= 32 nonzeros
-static void *pick_lane(const ps_csr_t *csr, int loss, int pen, bool literal, int km)
-{
-    bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
-    if (f64 && i64) return kernel_ptr_lane<double, long long>(loss, pen, literal, km);
-    if (f64) return kernel_ptr_lane<double, int>(loss, pen, literal, km);
-    if (i64) return kernel_ptr_lane<float, long long>(loss, pen, literal, km);
-    return kernel_ptr_lane<float, int>(loss, pen, literal, km);
 }
 static void *pick_hot(const ps_csr_t *csr, int loss, int pen, bool literal, int nc)
 {
@@ -1733,7 +1708,7 @@ static int hot2_ncopy(int flags)
 struct LaunchCfg {
     int ncopy = 1;
     void *kernel;
-    bool fast, hot2, lane = false;
+    bool fast, hot2;
     int ctas, wpc, smem_flag, stride, M, GB, H, hot_doubles;
     size_t smem;
     int64_t gscratch_bytes;
@@ -1829,22 +1804,6 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
             }
         }
     }
-    if ((sched->flags & PS_FLAG_LANE) && !det && part->kind == PS_PART_SINGLETON && part->max_slots <= 32 &&
-        sched->batch <= 0 && csr->n_rows < (int64_t(1) << 32) && L->H <= HOT_MAX) {
-        // one thread per in-flight sample (lane.cuh): warps_per_cta warps per CTA (default 4), one CTA per SM
-        L->lane = true;
-        L->fast = true;
-        L->hot2 = false;
-        L->wpc = wpc = sched->warps_per_cta > 0 ? std::min(sched->warps_per_cta, 8) : 4;
-        L->kernel = pick_lane(csr, prm ? prm->loss : PS_LOSS_LOGISTIC, pen, (sched->flags & PS_FLAG_DELTA_ZERO) != 0,
-                              part->max_slots);
-        L->ncopy = 1;
-        L->hot_doubles = L->H > 0 ? hot2_doubles(L->H, 1) : 0;
-        L->smem = (size_t)L->hot_doubles * 8;
-        L->smem_flag = 0;
-        L->stride = L->M = L->GB = 0;
-        L->gscratch_bytes = 0;
-    }
     if (L->smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(L->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem);
         if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run smem attribute");
@@ -1856,7 +1815,7 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
     // default grid: one full wave, but no more than n/16 warps in flight so a
     // sample is rarely processed twice concurrently on small problems
     int64_t cap = std::max<int64_t>(1, csr->n_rows / (16 * (int64_t)wpc));
-    L->ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas : (int)std::min<int64_t>((int64_t)sms * (L->lane ? 1 : per_sm), cap));
+    L->ctas = det ? 1 : (sched->ctas > 0 ? sched->ctas : (int)std::min<int64_t>((int64_t)sms * per_sm, cap));
     if (L->stride > 0 && !L->smem_flag) L->gscratch_bytes = (int64_t)L->stride * 8 * wpc * L->ctas;
     return PS_OK;
 }
@@ -1947,13 +1906,10 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     }
     // default flush period: 24 updates per warp for the singleton fast kernel
     // (32 warps per CTA), 16 elsewhere (tools/exp_floor2.py sweeps)
-    a.period = sched->hot_period > 0 ? sched->hot_period
-                                     : (L.lane ? 1 : ((L.fast && part->kind == PS_PART_SINGLETON && L.wpc == FAST_T / 32) ? 24 : 16));
+    a.period = sched->hot_period > 0 ? sched->hot_period : ((L.fast && part->kind == PS_PART_SINGLETON && L.wpc == FAST_T / 32) ? 24 : 16);
     // effective delay: in-flight warps + the staleness of the hot snapshot
-    // (up to period * ctas updates between a CTA's refreshes); the lane kernel
-    // has 32 samples in flight per warp and flushes every `period` rounds of 32
-    double tau = L.lane ? (double)L.ctas * L.wpc * 32.0 + (a.H > 0 ? 32.0 * a.period * L.ctas : 0.0)
-                        : (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);
+    // (up to period * ctas updates between a CTA's refreshes)
+    double tau = (double)((int64_t)L.ctas * L.wpc) + (a.H > 0 ? (double)a.period * L.ctas : 0.0);
     a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
     {  // diagnostics: flags bits 8..15 = extra divisor of the hot columns' kappa
         int div = (sched->flags >> 8) & 0xff;
@@ -1978,7 +1934,7 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     // (sps_hot_kernel: only up to 512 staged columns -- with 1024 the members'
     // second-hand tier-2 refresh measured unstable on a config-3-like
     // instance, tools/gpu/dbg_knobs.py, and round 1 measured no gain there)
-    if (L.fast && !L.lane && part->kind == PS_PART_SINGLETON && a.H > 0 && !(sched->flags & PS_FLAG_NO_CLUSTER) &&
+    if (L.fast && part->kind == PS_PART_SINGLETON && a.H > 0 && !(sched->flags & PS_FLAG_NO_CLUSTER) &&
         L.ctas % 2 == 0 && !(L.hot2 && a.H > 512)) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(L.ctas);
