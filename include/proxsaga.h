@@ -131,6 +131,10 @@ typedef struct ps_sched {
                                      reference's literal scatter_add (asynchronous.py:105-107);
                                      default: store 0 */
 /* bits 8..15: extra divisor of the staged columns' contention scale */
+#define PS_FLAG_MON_DEVICE_X 524288 /* ps_run_monitored: snaps is DEVICE memory of max_snaps*p doubles and
+                                        receives x only (stride 1), copied by a few CTAs beside the solve,
+                                        whose default grid leaves them their SMs (host snapshots of a large
+                                        problem's records take longer than an epoch over PCIe) */
 #define PS_FLAG_MON_ENDS_IN_PLACE 65536 /* ps_run_monitored: skip the copies of the first and last
                                            snapshots (the caller reads coord itself) */
 #define PS_FLAG_ZERO_IMMEDIATE 131072 /* fast kernel: a staged coordinate the prox zeroes is stored by
@@ -280,7 +284,9 @@ int ps_state_reset(double *coord, int64_t p, double *alpha, int64_t n, unsigned 
  * *n_snaps <= max_snaps.  The solve never stops for a checkpoint.  With
  * PS_FLAG_MON_ENDS_IN_PLACE in sched->flags, snaps[0] and the last snapshot
  * are not copied (their counts and times are still reported): the caller
- * evaluates those two states on coord itself, before and after the call. */
+ * evaluates those two states on coord itself, before and after the call.
+ * With PS_FLAG_MON_DEVICE_X, snaps is device memory and each snapshot is x
+ * only (p doubles). */
 int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm, double *coord,
                      double *alpha, const ps_sched_t *sched, void *scratch, void *stream, int64_t every,
                      int32_t max_snaps, double *snaps, int64_t *snap_counts, float *snap_ms, int32_t *n_snaps);

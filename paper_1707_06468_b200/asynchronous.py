@@ -9,9 +9,10 @@ counter-based sampler, reads x / abar inconsistently and commits with REDs /
 atomic exchanges (hot columns through per-CTA staging).  The monitor
 (:187-198) is the live one: ONE launch for the whole solve, a progress
 counter bumped every 16 updates of a warp, and at each checkpoint mark a
-copy-engine snapshot of the running solve (ps_run_monitored); the
-stop-the-world schedule (one launch per segment) remains for snapshots that
-would not fit in host memory and for distance tracking.
+copy-engine snapshot of the running solve (ps_run_monitored) -- for very
+large problems an x-only device snapshot copied by a few CTAs beside the
+solve; the stop-the-world schedule (one launch per segment) remains for
+snapshots that fit neither and for distance tracking.
 
 ``config.threads == 1`` replays worker 0's reference sample stream on a single
 warp, so a 1-thread run equals ``run_sequential`` bit for bit, as in the
@@ -106,12 +107,19 @@ def run_async(data, loss, penalty, partition, config, index=None, track_distance
         trace.append(it, n, obj, time.perf_counter() - start, distance=dist, threads=config.threads)
 
     nseg = -(-total // every)
-    if not single and not track and dp.p_dev * 32 * (nseg + 2) <= (4 << 30):
+    dev_snaps = False
+    if not single and not track and dp.p_dev * 32 * (nseg + 2) > (4 << 30):
+        # host snapshots of every record would not fit (or not keep pace): x-only
+        # device snapshots when a quarter of the free device memory holds them
+        free = dp.torch.cuda.mem_get_info(dp.device)[0]
+        dev_snaps = dp.p_dev * 8 * (nseg + 2) <= free // 4
+    if not single and not track and (dev_snaps or dp.p_dev * 32 * (nseg + 2) <= (4 << 30)):
         # the reference's live monitor: one launch, inconsistent snapshots of the
         # running solve at the checkpoint marks (ps_run_monitored); checkpoint 0
         # is evaluated on the device ahead of the launch
         its, objs, secs = dp.run_async_monitored(total, every, gamma, seed=config.seed, ctas=ctas,
-                                                 warps_per_cta=wpc, contention=config.contention)
+                                                 warps_per_cta=wpc, contention=config.contention,
+                                                 device_snaps=dev_snaps)
         for it, ob, sc in zip(its, objs, secs):
             trace.append(it, n, ob, sc, threads=config.threads)
         done = total

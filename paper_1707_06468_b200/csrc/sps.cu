@@ -1975,6 +1975,17 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     return PS_OK;
 }
 
+// x of the live coordinate records into a device snapshot (the monitor's
+// device mode: a few CTAs beside the solve, which leaves them the SMs)
+namespace ps {
+constexpr int SNAP_CTAS = 8;
+__global__ void __launch_bounds__(1024) k_snap_x(const double *coord, double *dst, int64_t p)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
+        dst[j] = __ldcg(coord + 4 * j);
+}
+}  // namespace ps
+
 // ---------------------------------------------------------------------------
 // ps_run_monitored: the reference's monitor (asynchronous.py:187-198) on the
 // device.  One asynchronous launch runs the whole solve; this (host) thread
@@ -2036,6 +2047,27 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     cudaEvent_t ev0 = m.ev0;
     std::vector<cudaEvent_t> &evs = m.evs;
     unsigned long long *h_cnt = m.h_cnt;
+    // device mode (PS_FLAG_MON_DEVICE_X): x-only snapshots into device memory by
+    // k_snap_x on SNAP_CTAS SMs the solve leaves free (host snapshots of all the
+    // records of a 3e7-coordinate problem cost more PCIe time than an epoch)
+    const bool dev_x = (sched->flags & PS_FLAG_MON_DEVICE_X) != 0;
+    ps_sched_t s2 = *sched;
+    if (dev_x && s2.ctas <= 0) {
+        int32_t c0 = 0, w0 = 0;
+        int64_t sb = 0;
+        int r0 = ps_launch_config(csr, part, sched, &c0, &w0, &sb);
+        if (r0) return r0;
+        s2.ctas = std::max(2, (c0 - SNAP_CTAS) & ~1);
+    }
+    const int64_t rec = dev_x ? 1 : 4;  // doubles per coordinate in a snapshot
+    auto snapshot = [&](int k, cudaStream_t on) -> cudaError_t {
+        if (dev_x) {
+            k_snap_x<<<SNAP_CTAS, 1024, 0, on>>>(coord, snaps + (size_t)k * p, p);
+            return cudaGetLastError();
+        }
+        return cudaMemcpyAsync(snaps + (size_t)k * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, on);
+    };
+    (void)rec;
     MCK(cudaMemsetAsync(sched->counter, 0, sizeof(unsigned long long), st), "monitor counter reset");
     MCK(cudaEventRecord(ev0, st), "monitor event");
     const bool ends_in_place = (sched->flags & PS_FLAG_MON_ENDS_IN_PLACE) != 0;
@@ -2045,14 +2077,14 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
         MCK(cudaEventRecord(evs[0], st), "monitor event");
     } else {
         MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
-        MCK(cudaMemcpyAsync(snaps, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, cp), "monitor snapshot");
+        MCK(snapshot(0, cp), "monitor snapshot");
         MCK(cudaEventRecord(evs[0], cp), "monitor event");
         // the solve must not start before snapshot 0 is taken
         MCK(cudaStreamWaitEvent(st, evs[0], 0), "monitor wait");
     }
     snap_counts[0] = 0;
     ns = 1;
-    int r = ps_run(csr, part, prm, coord, alpha, sched, scratch, stream);
+    int r = ps_run(csr, part, prm, coord, alpha, &s2, scratch, stream);
     if (r) return r;
     int64_t next_mark = every;
     while (true) {
@@ -2063,9 +2095,7 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
         MCK(cudaStreamSynchronize(poll), "monitor poll");
         const int64_t c = (int64_t)*h_cnt;
         if (c >= next_mark && next_mark < total && ns < max_snaps - 1) {
-            MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost,
-                                cp),
-                "monitor snapshot");
+            MCK(snapshot(ns, cp), "monitor snapshot");
             MCK(cudaEventRecord(evs[ns], cp), "monitor event");
             snap_counts[ns++] = c;
             while (next_mark <= c) next_mark += every;
@@ -2074,9 +2104,7 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     // final checkpoint: after the launch (consistent)
     MCK(cudaStreamWaitEvent(cp, ev0, 0), "monitor wait");
     MCK(cudaStreamSynchronize(st), "monitor join");
-    if (!ends_in_place)
-        MCK(cudaMemcpyAsync(snaps + (size_t)ns * 4 * p, coord, sizeof(double) * 4 * p, cudaMemcpyDeviceToHost, st),
-            "monitor snapshot");
+    if (!ends_in_place) MCK(snapshot(ns, st), "monitor snapshot");
     MCK(cudaEventRecord(evs[ns], st), "monitor event");
     if (ends_in_place) {
         // the last checkpoint comes after the launch AND after every snapshot copy

@@ -335,7 +335,7 @@ class DeviceProblem:
         self.slot_base += int(count)
 
     def run_async_monitored(self, total, every, gamma, seed=0, batch=0, ctas=0, warps_per_cta=0, contention=4.0,
-                            hot=None, hot_period=0, flags=0, gap=False):
+                            hot=None, hot_period=0, flags=0, gap=False, device_snaps=False):
         """`total` lock-free updates in ONE launch with the reference's live
         monitor (asynchronous.py:181-198, ps_run_monitored): each time the
         progress counter crosses a multiple of `every`, the live coordinate
@@ -345,8 +345,11 @@ class DeviceProblem:
         its snapshot's device time plus one measured objective evaluation (the
         time the monitor would need to know it).  Checkpoint 0 (the starting
         state) and the last one (the consistent state after the launch) are
-        evaluated in place, without a copy.  Returns (iterations,
-        objectives, seconds[, duals])."""
+        evaluated in place, without a copy.  ``device_snaps``: x-only snapshots
+        into device memory, copied by a few CTAs beside the solve (whose default
+        grid leaves them their SMs; PS_FLAG_MON_DEVICE_X) -- for problems whose
+        records would take longer than an epoch to copy to the host.  Returns
+        (iterations, objectives, seconds[, duals])."""
         torch = self.torch
         if hot is None:
             hot = self.part_kind == "singleton"
@@ -354,9 +357,12 @@ class DeviceProblem:
         # checkpoint 0 and the final one are evaluated in place (below): no copies of them
         sched = self._sched(total, seed=seed, batch=batch, ctas=ctas, warps_per_cta=warps_per_cta,
                             contention=contention, hot=hot, hot_period=hot_period,
-                            flags=flags | _lib.FLAG_MON_ENDS_IN_PLACE)
+                            flags=flags | _lib.FLAG_MON_ENDS_IN_PLACE | (_lib.FLAG_MON_DEVICE_X if device_snaps else 0))
         scr = self._scratch_for(sched)
-        snaps = torch.empty((nmax, self.p_dev, 4), dtype=torch.float64, pin_memory=True)  # DMA targets
+        if device_snaps:
+            snaps = torch.empty((nmax, self.p_dev), dtype=torch.float64, device=self.device)  # x only
+        else:
+            snaps = torch.empty((nmax, self.p_dev, 4), dtype=torch.float64, pin_memory=True)  # DMA targets
         counts = (ctypes.c_int64 * nmax)()
         ms = (ctypes.c_float * nmax)()
         ns = ctypes.c_int32(0)
@@ -382,8 +388,11 @@ class DeviceProblem:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         buf = None
         for j in range(1, k):
+            stride = 4
             if j == k - 1:
                 ptr = self.coord.data_ptr()  # the final snapshot is the (consistent) state after the launch
+            elif device_snaps:
+                ptr, stride = snaps[j].data_ptr(), 1
             else:
                 if buf is None:
                     buf = torch.empty((self.p_dev, 4), dtype=torch.float64, device=self.device)
@@ -391,12 +400,12 @@ class DeviceProblem:
                 ptr = buf.data_ptr()
             if j == 1:
                 e0.record()
-            _lib.check(L.ps_objective(self.csr, self.part, self.params(), ptr, 4, outs[j].data_ptr(),
+            _lib.check(L.ps_objective(self.csr, self.part, self.params(), ptr, stride, outs[j].data_ptr(),
                                       _lib.stream_ptr()))
             if j == 1:
                 e1.record()
             if gap:
-                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), ptr, 4, duals[j].data_ptr(),
+                _lib.check(L.ps_dual_objective(self.csr, self.part, self.params(), ptr, stride, duals[j].data_ptr(),
                                                _lib.stream_ptr()))
         o = outs[:k].cpu().numpy()  # synchronizes
         t_eval = e0.elapsed_time(e1) / 1e3 if k > 1 else 0.0

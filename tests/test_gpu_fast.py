@@ -205,18 +205,24 @@ def test_checkpointed_duality_gap(cuda):
     assert dual == pytest.approx(duals[-1], rel=1e-12)
 
 
-def test_live_monitor_checkpoints(cuda):
+@pytest.mark.parametrize("device_snaps", [False, True], ids=["host_snapshots", "device_x_snapshots"])
+def test_live_monitor_checkpoints(cuda, device_snaps):
     """run_async_monitored (ps_run_monitored): one launch, snapshots of the
     running solve at the epoch marks; counters and device times increase,
     the first checkpoint is x0, the last the state after the launch, and the
-    solve reaches the optimum; the final objective equals the live one."""
+    solve reaches the optimum; the final objective equals the live one.
+    device_x_snapshots: x-only device snapshots copied by a few CTAs beside
+    the solve (PS_FLAG_MON_DEVICE_X), the mode for configs 3/4."""
     data = _instance(20)
     lam = 1.0 / data.n_samples
     dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
                        drop_dead_blocks=True)
     gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
     fref = _fstar(dp, gamma)
-    its, objs, secs, duals = dp.run_async_monitored(60 * dp.n, dp.n, gamma, seed=3, gap=True)
+    its, objs, secs, duals = dp.run_async_monitored(60 * dp.n, dp.n, gamma, seed=3, gap=True,
+                                                    device_snaps=device_snaps)
+    if device_snaps:  # the middle checkpoints' objectives fall towards the optimum
+        assert len(its) >= 10 and objs[1] < objs[0] and objs[len(objs) // 2] < objs[1]
     assert its[0] == 0 and its[-1] == 60 * dp.n and len(its) >= 3
     assert all(b >= a for a, b in zip(its, its[1:]))
     assert all(b >= a for a, b in zip(secs[1:], secs[2:]))
