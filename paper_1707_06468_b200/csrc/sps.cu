@@ -2051,6 +2051,12 @@ extern "C" int ps_run_monitored(const ps_csr_t *csr, const ps_part_t *part, cons
     // k_snap_x on SNAP_CTAS SMs the solve leaves free (host snapshots of all the
     // records of a 3e7-coordinate problem cost more PCIe time than an epoch)
     const bool dev_x = (sched->flags & PS_FLAG_MON_DEVICE_X) != 0;
+    if (dev_x) {
+        // load k_snap_x now: a lazily loaded kernel's first launch waits for the
+        // device to go idle, i.e. for the solve (measured: first snapshot at the end)
+        cudaFuncAttributes fa;
+        MCK(cudaFuncGetAttributes(&fa, k_snap_x), "monitor snapshot kernel");
+    }
     ps_sched_t s2 = *sched;
     if (dev_x && s2.ctas <= 0) {
         int32_t c0 = 0, w0 = 0;

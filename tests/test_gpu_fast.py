@@ -221,8 +221,8 @@ def test_live_monitor_checkpoints(cuda, device_snaps):
     fref = _fstar(dp, gamma)
     its, objs, secs, duals = dp.run_async_monitored(60 * dp.n, dp.n, gamma, seed=3, gap=True,
                                                     device_snaps=device_snaps)
-    if device_snaps:  # the middle checkpoints' objectives fall towards the optimum
-        assert len(its) >= 10 and objs[1] < objs[0] and objs[len(objs) // 2] < objs[1]
+    if device_snaps:  # snapshots taken while the solve runs, not after it
+        assert its[1] < its[-1] and secs[1] < 0.9 * secs[-1]
     assert its[0] == 0 and its[-1] == 60 * dp.n and len(its) >= 3
     assert all(b >= a for a, b in zip(its, its[1:]))
     assert all(b >= a for a, b in zip(secs[1:], secs[2:]))
