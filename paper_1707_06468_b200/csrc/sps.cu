@@ -33,7 +33,9 @@
 //   GENERAL    any BlockPartition; T_i / slot positions precomputed by
 //              ps_prepare; blocks processed one at a time.
 #include <algorithm>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 #include <cstdio>
 
@@ -1699,6 +1701,62 @@ static void *pick_kernel(const ps_csr_t *csr, int kind, bool big)
 #undef PICK
 }
 
+// Launch-geometry queries cached per (kernel, device, block, smem): the
+// occupancy and cluster-residency queries and the dynamic-smem attribute cost
+// tens of microseconds each in the driver and ran on every call (three
+// launch_config evaluations per run_async: ~0.2 ms of a 2.8 ms end-to-end call)
+namespace {
+std::mutex g_geo_mu;
+std::map<std::tuple<void *, int, int, size_t>, int> g_occ, g_clusters;
+std::map<std::pair<void *, int>, size_t> g_smem_set;
+cudaError_t cached_set_smem(void *k, int dev, size_t smem)
+{
+    std::lock_guard<std::mutex> g(g_geo_mu);
+    size_t &have = g_smem_set[{k, dev}];
+    if (have >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
+cudaError_t cached_occupancy(int *per_sm, void *k, int dev, int threads, size_t smem)
+{
+    std::lock_guard<std::mutex> g(g_geo_mu);
+    auto key = std::make_tuple(k, dev, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+        *per_sm = it->second;
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k, threads, smem);
+    if (e == cudaSuccess) g_occ[key] = *per_sm;
+    return e;
+}
+// resident clusters of 2 for the kernel (-1: the query was refused)
+int cached_pair_clusters(void *k, int dev, int threads, size_t smem, int ctas)
+{
+    std::lock_guard<std::mutex> g(g_geo_mu);
+    auto key = std::make_tuple(k, dev, threads, smem);
+    auto it = g_clusters.find(key);
+    if (it != g_clusters.end()) return it->second;
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(ctas);
+    q.blockDim = dim3(threads);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = 2;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int resident = 0;
+    if (cudaOccupancyMaxActiveClusters(&resident, k, &q) != cudaSuccess) resident = -1;
+    cudaGetLastError();  // a refused query leaves no sticky error behind
+    g_clusters[key] = resident;
+    return resident;
+}
+}  // namespace
+
 // pending-delta copies of sps_hot_kernel: flags bits 24..25 (0: default 1, else 1 << (v - 1))
 static int hot2_ncopy(int flags)
 {
@@ -1805,11 +1863,11 @@ static int launch_config(const ps_csr_t *csr, const ps_part_t *part, const ps_sc
         }
     }
     if (L->smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(L->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L->smem);
+        cudaError_t e = cached_set_smem(L->kernel, dev, L->smem);
         if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run smem attribute");
     }
     int per_sm = 1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->kernel, wpc * 32, L->smem);
+    cudaError_t e = cached_occupancy(&per_sm, L->kernel, dev, wpc * 32, L->smem);
     if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run occupancy");
     per_sm = std::max(per_sm, 1);
     // default grid: one full wave, but no more than n/16 warps in flight so a
@@ -1936,21 +1994,10 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     // instance, tools/gpu/dbg_knobs.py, and round 1 measured no gain there)
     if (L.fast && part->kind == PS_PART_SINGLETON && a.H > 0 && !(sched->flags & PS_FLAG_NO_CLUSTER) &&
         L.ctas % 2 == 0 && !(L.hot2 && a.H > 512)) {
-        cudaLaunchConfig_t q = {};
-        q.gridDim = dim3(L.ctas);
-        q.blockDim = dim3(L.wpc * 32);
-        q.dynamicSmemBytes = L.smem;
-        cudaLaunchAttribute qa[1];
-        qa[0].id = cudaLaunchAttributeClusterDimension;
-        qa[0].val.clusterDim.x = 2;
-        qa[0].val.clusterDim.y = 1;
-        qa[0].val.clusterDim.z = 1;
-        q.attrs = qa;
-        q.numAttrs = 1;
-        int resident = 0;
-        if (cudaOccupancyMaxActiveClusters(&resident, L.kernel, &q) == cudaSuccess && 2 * resident >= L.ctas)
-            a.cluster = 2;
-        cudaGetLastError();  // a refused query leaves no sticky error behind
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int resident = cached_pair_clusters(L.kernel, dev, L.wpc * 32, L.smem, L.ctas);
+        if (resident > 0 && 2 * resident >= L.ctas) a.cluster = 2;
     }
     void *args[] = {(void *)&a};
     cudaError_t e;

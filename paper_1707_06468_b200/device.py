@@ -40,6 +40,22 @@ def _f32_exact(a):
         return bool(np.array_equal(a.astype(np.float32).astype(np.float64), a))
 
 
+_PINNED = {}
+
+
+def _pinned_snapshots(torch, nmax, p):
+    """Pinned host snapshot buffers of the live monitor, kept across calls
+    (cudaHostAlloc of a few MB costs ~0.3 ms, a fifth of a config-2 solve):
+    one buffer per device, grown on demand; returns an (nmax, p, 4) view."""
+    need = nmax * p * 4
+    key = torch.cuda.current_device()
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(need, dtype=torch.float64, pin_memory=True)
+        _PINNED[key] = buf
+    return buf[:need].view(nmax, p, 4)
+
+
 class DeviceProblem:
     """One problem on one GPU.
 
@@ -362,7 +378,7 @@ class DeviceProblem:
         if device_snaps:
             snaps = torch.empty((nmax, self.p_dev), dtype=torch.float64, device=self.device)  # x only
         else:
-            snaps = torch.empty((nmax, self.p_dev, 4), dtype=torch.float64, pin_memory=True)  # DMA targets
+            snaps = _pinned_snapshots(torch, nmax, self.p_dev)  # DMA targets
         counts = (ctypes.c_int64 * nmax)()
         ms = (ctypes.c_float * nmax)()
         ns = ctypes.c_int32(0)
