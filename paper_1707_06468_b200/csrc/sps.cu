@@ -741,6 +741,141 @@ __global__ void __launch_bounds__(MAXT) sps_kernel(const KArgs a)
 
 
 // ---------------------------------------------------------------------------
+// Deterministic replay with the whole state on chip (SINGLETON rows of <= 64
+// nonzeros, 3p + n doubles within the shared-memory budget: BASELINE config 1
+// and the reference tests' problems).  The same arithmetic, in the same order,
+// as row_reg's deterministic path (so the iterates are bit-identical to the
+// global-memory replay, which matches the reference's to ~1e-15): x, abar, D
+// and alpha live in shared memory for the whole call, so a step needs no
+// global stores and no fence -- only a __syncwarp -- and the next step's row
+// is fetched while the current one computes.  One warp; the state is written
+// back at the end.
+struct DetRow {
+    int64_t i;
+    double y;
+    int col[2];
+    double val[2];
+};
+template <typename VT, typename PT>
+__global__ void __launch_bounds__(32) sps_det_smem_kernel(const KArgs a)
+{
+    extern __shared__ double smem_dyn[];
+    const int lane = threadIdx.x & 31;
+    const int64_t p = a.p, n = a.n, count = a.count;
+    double *const sx = smem_dyn, *const sab = sx + p, *const sdd = sab + p, *const sal = sdd + p;
+    for (int64_t j = lane; j < p; j += 32) {
+        sx[j] = a.coord[4 * j];
+        sab[j] = a.coord[4 * j + 1];
+        sdd[j] = a.coord[4 * j + 2];
+    }
+    for (int64_t i = lane; i < n; i += 32) sal[i] = a.alpha[i];
+    __syncwarp();
+    constexpr int NCH = 2;
+    // samples, row extents and labels of 32 steps at a time (lane L: step t0 + L):
+    // one dependent round trip per 32 steps instead of three per step
+    int64_t ci = 0, clo = 0, ni = 0, nlo = 0;
+    int ck = 0, nk = 0;
+    double cy = 0.0, ny = 0.0;
+    auto batch = [&](int64_t t0, int64_t &bi, int64_t &blo, int &bk, double &by) {
+        const int64_t t = t0 + lane;
+        bi = blo = 0;
+        bk = 0;
+        by = 0.0;
+        if (t < count) {
+            bi = __ldg(a.samples + t);
+            blo = rp<PT>(a.row_ptr, bi);
+            bk = (int)(rp<PT>(a.row_ptr, bi + 1) - blo);
+            by = rv<VT>(a.y, bi);
+        }
+    };
+    batch(0, ci, clo, ck, cy);
+    batch(32, ni, nlo, nk, ny);
+    // the row of step tt (fetched in order, two steps before it is used)
+    auto fetch = [&](int64_t tt, DetRow &r) {
+        if ((tt & 31) == 0 && tt > 0) {
+            ci = ni;
+            clo = nlo;
+            ck = nk;
+            cy = ny;
+            batch(tt + 32, ni, nlo, nk, ny);
+        }
+        const int src = (int)(tt & 31);
+        r.i = __shfl_sync(FULL, ci, src);
+        r.y = __shfl_sync(FULL, cy, src);
+        const int64_t lo = __shfl_sync(FULL, clo, src);
+        const int k = tt < count ? __shfl_sync(FULL, ck, src) : 0;
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            const int e = c * 32 + lane;
+            r.col[c] = e < k ? __ldg(a.col + lo + e) : -1;
+            r.val[c] = e < k ? rv<VT>(a.val, lo + e) : 0.0;
+        }
+    };
+    DetRow r0, r1, r2;
+    fetch(0, r0);
+    fetch(1, r1);
+    for (int64_t t = 0; t < count; t++) {
+        fetch(t + 2, r2);
+        // ---- the step (row_reg's deterministic arithmetic, same order)
+        const int64_t i = r0.i;
+        double xr[NCH], abr[NCH], dr[NCH];
+        double part = 0.0;
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            if (r0.col[c] >= 0) {
+                xr[c] = sx[r0.col[c]];
+                abr[c] = sab[r0.col[c]];
+                dr[c] = sdd[r0.col[c]];
+                part += r0.val[c] * xr[c];
+            }
+        }
+        double old = 0.0;
+        if (lane == 0) old = sal[i];
+        old = __shfl_sync(FULL, old, 0);
+        const double margin = warp_sum(part);
+        const double nw = loss_deriv(a.loss, margin, r0.y);
+        const double ds = nw - old;
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            if (r0.col[c] >= 0) {
+                double v = dr[c] * (abr[c] + a.lambda1 * xr[c]);
+                v += ds * r0.val[c];
+                const double g = step_of(a, dr[c]);
+                const double u = xr[c] - g * v;
+                const double z = prox_sep(a.pen, u, g * dr[c], a.lam2, a.lo, a.hi);
+                if (a.trace_v) {
+                    a.trace_v[r0.col[c]] = v;
+                    a.trace_dx[r0.col[c]] = z - xr[c];
+                }
+                sx[r0.col[c]] = xr[c] + (z - xr[c]);
+            }
+        }
+        if (lane == 0) sal[i] = nw;
+        const double tq = (nw - old) / a.n_d;
+#pragma unroll
+        for (int c = 0; c < NCH; c++)
+            if (r0.col[c] >= 0) sab[r0.col[c]] = abr[c] + tq * r0.val[c];
+        __syncwarp();
+        r0 = r1;
+        r1 = r2;
+    }
+    for (int64_t j = lane; j < p; j += 32) {
+        a.coord[4 * j] = sx[j];
+        a.coord[4 * j + 1] = sab[j];
+    }
+    for (int64_t q = lane; q < n; q += 32) a.alpha[q] = sal[q];
+}
+template <typename VT, typename PT> static void *det_smem_ptr() { return (void *)sps_det_smem_kernel<VT, PT>; }
+static void *pick_det_smem(const ps_csr_t *csr)
+{
+    const bool f64 = csr->value_type == PS_F64, i64 = csr->row_ptr_type == PS_I64;
+    if (f64 && i64) return det_smem_ptr<double, long long>();
+    if (f64) return det_smem_ptr<double, int>();
+    if (i64) return det_smem_ptr<float, long long>();
+    return det_smem_ptr<float, int>();
+}
+
+// ---------------------------------------------------------------------------
 // Fast async kernel: SINGLETON rows of <= 32 nonzeros (BASELINE configs 2-4).
 // Same per-update arithmetic as row_reg, specialised on loss / penalty, with
 // a software pipeline across updates:
@@ -2001,6 +2136,21 @@ extern "C" int ps_run(const ps_csr_t *csr, const ps_part_t *part, const ps_param
     }
     void *args[] = {(void *)&a};
     cudaError_t e;
+    // deterministic replay with the state on chip (sps_det_smem_kernel)
+    const size_t det_smem = (size_t)(3 * csr->n_cols + csr->n_rows) * sizeof(double);
+    if (det && part->kind == PS_PART_SINGLETON && part->max_slots <= 64 && prm->penalty != PS_PEN_GROUP &&
+        det_smem <= 200 * 1024 && !(sched->flags & PS_FLAG_GENERIC)) {
+        void *k = pick_det_smem(csr);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (det_smem > 48 * 1024) {
+            e = cached_set_smem(k, dev, det_smem);
+            if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run det smem attribute");
+        }
+        e = cudaLaunchKernel(k, dim3(1), dim3(32), args, det_smem, (cudaStream_t)stream);
+        if (e != cudaSuccess) return ps_cuda_fail(e, "ps_run launch");
+        return PS_OK;
+    }
     if (a.cluster > 1) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.ctas);
