@@ -56,6 +56,9 @@ struct BArgs {
 };
 
 constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
+#ifndef BATCH_MINB
+#define BATCH_MINB 1
+#endif
 // State layout: states are grouped S = 2 at a time (one 32-B sector per
 // coordinate and group); group g of the B states is its own region
 //   state[((g * NB*G + j) * S + beta % S) * 2 + {0: x, 1: abar}],  g = beta / S
@@ -93,7 +96,7 @@ __device__ __forceinline__ double *rep_ptr(const BArgs &a, int rr, int rank, int
 }
 
 template <typename VT, int LOSS, int B, int GT, bool REP>
-__global__ void __launch_bounds__(BATCH_T) sps_group_batch_kernel(const BArgs a)
+__global__ void __launch_bounds__(BATCH_T, BATCH_MINB) sps_group_batch_kernel(const BArgs a)
 {
     constexpr int LPB = 32 / B;                                  // lanes per state
     constexpr int S = B < BATCH_S ? B : BATCH_S;                 // states per layout group
