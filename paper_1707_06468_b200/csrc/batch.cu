@@ -56,8 +56,11 @@ struct BArgs {
 };
 
 constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
-#ifndef BATCH_MINB
-#define BATCH_MINB 1
+// A/B knob: -DBATCH_MINB=2 caps the kernel at 64 registers (two CTAs per SM)
+#ifdef BATCH_MINB
+#define BATCH_BOUNDS __launch_bounds__(BATCH_T, BATCH_MINB)
+#else
+#define BATCH_BOUNDS __launch_bounds__(BATCH_T)
 #endif
 // State layout: states are grouped S = 2 at a time (one 32-B sector per
 // coordinate and group); group g of the B states is its own region
@@ -96,7 +99,7 @@ __device__ __forceinline__ double *rep_ptr(const BArgs &a, int rr, int rank, int
 }
 
 template <typename VT, int LOSS, int B, int GT, bool REP>
-__global__ void __launch_bounds__(BATCH_T, BATCH_MINB) sps_group_batch_kernel(const BArgs a)
+__global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
 {
     constexpr int LPB = 32 / B;                                  // lanes per state
     constexpr int S = B < BATCH_S ? B : BATCH_S;                 // states per layout group
