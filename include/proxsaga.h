@@ -147,6 +147,9 @@ typedef struct ps_sched {
                                       two pending copies) instead of sps_hot_kernel (A/B, diagnostics) */
 #define PS_FLAG_NO_CLUSTER 2097152 /* fast kernel: no CTA pairs (each CTA refreshes its hot snapshot
                                       from L2; default: clusters of 2 share one refresh) */
+#define PS_FLAG_LOCAL_VIEW 134217728 /* hot kernel: a staged commit also writes its prox result into the
+                                        CTA's snapshot (the CTA reads its own commits at once; opt-in,
+                                        DESIGN.md K2'' "local view") */
 
 int ps_abi_version(void);
 const char *ps_last_error(void);

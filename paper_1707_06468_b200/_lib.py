@@ -27,6 +27,7 @@ FLAG_SCRAMBLE, FLAG_GENERIC, FLAG_DELTA_ZERO, FLAG_GROUP_WARP, FLAG_GROUP_LANE =
 FLAG_MON_ENDS_IN_PLACE, FLAG_ZERO_IMMEDIATE, FLAG_GROUP_STORE_ZEROS = 65536, 131072, 262144
 FLAG_NO_CLUSTER, FLAG_FAST_V1 = 2097152, 4194304
 FLAG_MON_DEVICE_X = 524288
+FLAG_LOCAL_VIEW = 134217728
 ABI_VERSION = 2
 
 # Every symbol include/proxsaga.h declares (checked by tests/test_abi.py).

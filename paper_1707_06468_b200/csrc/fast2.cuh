@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
     double *const sd = smem_dyn + 2 * H;
     const int nc = a.ncopy;
     const bool diag_nohot = (a.diag & (1 << 26)) != 0;  // measurement only: staged deltas are dropped
+    const bool local_view = (a.diag & PS_FLAG_LOCAL_VIEW) != 0;  // opt-in: a staged commit also updates the CTA snapshot
     double *const pend = smem_dyn + 3 * H;
     unsigned *const zf = reinterpret_cast<unsigned *>(pend + 2 * nc * H);
     // 32-bit shared addresses of the staging arrays; this warp's pending copy
@@ -356,6 +357,8 @@ __global__ void __launch_bounds__(1024, 1) sps_hot_kernel(const KArgs a)
                 if (defer) sh_st32(a_zf + 4u * sl, 1u);
                 if (hot && !z0 && !diag_nohot) sh_add(d_px + sl, z - xh[c]);
                 if (hot) sh_st32(a_dirty + 4u * sl, 1u);  // after the pending add / zero flag (flush order)
+                if (hot && local_view)  // the CTA reads its own commit at once (racy plain store; a refresh overwrites it)
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a_snap + 16u * sl), "d"(z) : "memory");
                 pcol[c] = hot ? -2 - (int)sl : col[c];
                 pval[c] = cval;
             }

@@ -77,4 +77,5 @@ def test_flag_constants_match_header():
                     "GROUP_WARP": _lib.FLAG_GROUP_WARP, "GROUP_LANE": _lib.FLAG_GROUP_LANE,
                     "MON_ENDS_IN_PLACE": _lib.FLAG_MON_ENDS_IN_PLACE, "ZERO_IMMEDIATE": _lib.FLAG_ZERO_IMMEDIATE,
                     "GROUP_STORE_ZEROS": _lib.FLAG_GROUP_STORE_ZEROS, "NO_CLUSTER": _lib.FLAG_NO_CLUSTER,
-                    "FAST_V1": _lib.FLAG_FAST_V1, "MON_DEVICE_X": _lib.FLAG_MON_DEVICE_X}
+                    "FAST_V1": _lib.FLAG_FAST_V1, "MON_DEVICE_X": _lib.FLAG_MON_DEVICE_X,
+                    "LOCAL_VIEW": _lib.FLAG_LOCAL_VIEW}

@@ -51,8 +51,8 @@ def test_fast_kernel_layouts_converge(cuda, k, value_dtype):
     assert np.max(np.abs(live - dp.abar())) < 1e-12
 
 
-@pytest.mark.parametrize("ctas", [1, 2])
-def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas):
+@pytest.mark.parametrize("ctas,flags", [(1, 0), (2, 0), (1, 134217728), (2, 134217728)])
+def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas, flags):
     """One CTA (or one CTA pair) of the 32-warp staged hot kernel: 32-64 updates
     in flight, every staged mechanism active (snapshot, pending accumulators,
     dirty words, deferred zero stores, flushes, cluster refresh for the pair).
@@ -60,7 +60,8 @@ def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas):
     replay's optimum to 1e-16 (one CTA) / 1e-9 (a pair) -- a sharp check that no
     staged delta is lost or applied twice (a kernel variant that dropped or
     replayed pending deltas ended 2-7% above it here while still converging on
-    the full grid; K2'')."""
+    the full grid; K2'').  Also with PS_FLAG_LOCAL_VIEW (a staged commit
+    writes its result into the CTA snapshot)."""
     data = _instance(20)
     lam = 1.0 / data.n_samples
     dp = DeviceProblem(data, pb.Loss("logistic", lam), pb.L1Penalty(lam), pb.singleton_partition(data.n_features),
@@ -70,7 +71,7 @@ def test_hot_kernel_one_cta_reaches_the_replay_optimum(cuda, ctas):
     fref = _fstar(dp, gamma)
     for seed in (5, 6):
         dp.reset_state()
-        dp.run_async(60 * dp.n, gamma, seed=seed, ctas=ctas, warps_per_cta=32)
+        dp.run_async(60 * dp.n, gamma, seed=seed, ctas=ctas, warps_per_cta=32, flags=flags)
         f = dp.objective()
         assert abs(f - fref) <= 1e-8 * abs(fref), (seed, f, fref)
     live = dp.abar()
@@ -310,7 +311,8 @@ def test_fast_kernel_commit_variants_converge(cuda):
                        drop_dead_blocks=True)
     gamma = resolve_step_size("1/2L", dp.L, dp.n, lam)
     fref = _fstar(dp, gamma)
-    for fl in (0, _lib.FLAG_NO_CLUSTER, _lib.FLAG_ZERO_IMMEDIATE, _lib.FLAG_NO_CLUSTER | _lib.FLAG_ZERO_IMMEDIATE):
+    for fl in (0, _lib.FLAG_NO_CLUSTER, _lib.FLAG_ZERO_IMMEDIATE, _lib.FLAG_NO_CLUSTER | _lib.FLAG_ZERO_IMMEDIATE,
+               _lib.FLAG_LOCAL_VIEW):
         dp.reset_state()
         dp.run_async(60 * dp.n, gamma, seed=17, flags=fl)
         gap = (dp.objective() - fref) / abs(fref)
