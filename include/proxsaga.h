@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 2
+#define PS_ABI_VERSION 3
 
 enum ps_status { PS_OK = 0, PS_EINVAL = 1, PS_ERANGE = 2, PS_ECUDA = 3, PS_ENOMEM = 4 };
 /* losses.py:15-19 */
@@ -238,16 +238,24 @@ int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, const ps_params
                      int32_t B, double *state, double *alpha, const ps_sched_t *sched, double *xrep, int32_t nrep,
                      int32_t nrb, void *stream);
 /* doubles of a ps_batch_run state for p coordinates, blocks of G, B states
- * (regions of two states, each followed by the current region pad), and of the
+ * (regions of two states: the contiguous records, the scattered hot blocks' area, the pad), and of the
  * replica accumulators of ps_batch_run_rep */
 int64_t ps_batch_state_doubles(int64_t p, int32_t G, int32_t B);
 int64_t ps_batch_rep_doubles(int32_t nrep, int32_t nrb, int32_t G, int32_t B);
 /* diagnostics: the state's region pad and the replica chunk stride, in doubles
  * (process-wide; allocate states after setting them) */
 int ps_batch_tune(int64_t rpad, int64_t rstride);
-/* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state) */
-int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
-                   int32_t set, void *stream);
+/* diagnostics: the scattered hot blocks of the batched state -- the nhot most frequent stored
+ * blocks (stored index rank << hot_shift: ps_hot_layout's spread order) keep coordinate q in the
+ * region's hot area at (rank*G + q)*hstride doubles, one sector per hstride (defaults: 128 blocks
+ * from B = 8 and 32 below (nhot = -1), 128 doubles = 1 KB; nhot = 0 or hstride = 0: every block in
+ * the contiguous record).
+ * Process-wide; allocate states after setting */
+int ps_batch_tune2(int32_t nhot, int64_t hstride);
+/* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state);
+ * hot_shift = the ps_sched_t.hot_shift the state is run with (it places the scattered hot blocks) */
+int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t hot_shift, int32_t beta, int32_t field,
+                   double *vec, int32_t set, void *stream);
 
 /* losses.py:73-86 loss_scalar, elementwise: value[i] = l(z[i], b[i]) (overflow-safe
  * log1p forms) and deriv[i] = l'(z[i], b[i]), the deterministic kernels' arithmetic;

@@ -27,6 +27,12 @@
 
 namespace ps {
 
+// state layout (bidx below)
+struct BLay {
+    int64_t body, region, hstride;  // doubles: nb*G*S*2; body + hot area + pad; per scattered coordinate
+    int32_t G, S, hshift, nhot;
+};
+
 struct BArgs {
     const int32_t *row_ptr;
     const int32_t *col;
@@ -53,6 +59,7 @@ struct BArgs {
     double *xrep;
     int32_t nrep, nrb, hshift;
     int64_t rpad, rstride;  // state region pad; doubles per (replica, hot block) chunk
+    BLay L;                 // state layout (bidx)
 };
 
 constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
@@ -76,15 +83,31 @@ constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
 constexpr int BATCH_S = 2;
 constexpr int PROGRESS_BATCH_B = 16;           // rows per progress bump of a warp
 constexpr int BATCH_SM_WARP = 32 + 32 * 16;    // per-warp shared doubles: block ids + row values [32][16]
-// region g of the state starts at g * (nb*G*S*2 + rpad) doubles: the pad keeps
-// the regions' copies of a hot block from aliasing onto the same L2 slice
-__host__ __device__ __forceinline__ int64_t bidx(int64_t j, int beta, int64_t nb, int G, int S, int64_t rpad)
+// Region g of the state is [body | hot area | pad]: body = nb*G*S*2 doubles in
+// [block][q][S](x, abar) order.  SCATTERED HOT BLOCKS: stored block b with
+// (b & ((1 << hshift) - 1)) == 0 and rank r = b >> hshift < nhot (the most
+// frequent blocks of ps_hot_layout's spread order; the first nhot blocks when
+// hshift = 0) keeps its coordinates in the hot area instead, coordinate q at
+// (r*G + q) * hstride doubles -- one 32-B sector (the S states' (x, abar)
+// pairs) per hstride (1 KB).  Every row commits all G coordinates of the Zipf
+// head's blocks in every state; in the contiguous record four coordinates
+// share a line and the L2 serialises a line's atomics (measured, config 5,
+// tools/gpu/exp_batch_scatter.py: B = 16 24.9 -> 39.8 M rows/s, B = 8 25.3 ->
+// 63.3, B = 4 43.5 -> 84.5, B = 2 78.8 -> 115 -- more than the replica
+// accumulators gave, which it replaces by default).  The pad (diagnostics)
+// shifts the regions against each other.
+__host__ __device__ __forceinline__ int64_t bidx(int64_t b, int q, int beta, const BLay &L)
 {
-    return (int64_t)(beta / S) * rpad + (((int64_t)(beta / S) * nb * G + j) * S + beta % S) * 2;
+    const int64_t base = (int64_t)(beta / L.S) * L.region + (beta % L.S) * 2;
+    const int64_t r = b >> L.hshift;
+    if (r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0) return base + L.body + (r * L.G + q) * L.hstride;
+    return base + (b * L.G + q) * L.S * 2;
 }
 // layout knobs (doubles): the region pad and the stride of one (replica, hot
 // block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
 static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
+static int64_t g_hstride = 128;  // scattered hot blocks: one sector per KB (adjacent lines measured slower below B = 16)
+static int32_t g_nhot = -1;      // how many: -1 = by B (128 from B = 8, else 32: tools/gpu/exp_batch_scatter.py); ps_batch_tune2
 
 // rank of a replicated hot block, or -1
 template <bool REP> __device__ __forceinline__ int rep_rank(const BArgs &a, int64_t b)
@@ -150,7 +173,8 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
             const int e = sub + LPB * j;
             const int ce = __shfl_sync(FULL, col, e & 31);
-            xm[j] = (e < k) ? ld_cg(st + bidx(ce, beta, a.nb, G, S, a.rpad)) : 0.0;
+            const int be = ce / G;
+            xm[j] = (e < k) ? ld_cg(st + bidx(be, ce - be * G, beta, a.L)) : 0.0;
             const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
             if (rk >= 0)
                 for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
@@ -200,7 +224,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
-                v[r] = q < nq ? ld_cg2(st + bidx((int64_t)b * G + q, beta, a.nb, G, S, a.rpad)) : make_double2(0.0, 0.0);
+                v[r] = q < nq ? ld_cg2(st + bidx(b, q, beta, a.L)) : make_double2(0.0, 0.0);
                 if (rk >= 0 && q < nq)
                     for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
@@ -242,7 +266,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                 for (int r = 0; r < RMAX; r++) {
                     const int q = sub + LPB * r;
                     if (q < nq) {
-                        double *px = st + bidx((int64_t)b * G + q, beta, a.nb, G, S, a.rpad);
+                        double *px = st + bidx(b, q, beta, a.L);
                         const double z = u[r] * f;
                         if (a.det) {
                             *px = cur[r].x + (z - cur[r].x);
@@ -267,7 +291,8 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const int ce = __shfl_sync(FULL, col, e & 31);
             const double ve = __shfl_sync(FULL, val, e & 31);
             if (e < k) {
-                double *pab = st + bidx(ce, beta, a.nb, G, S, a.rpad) + 1;
+                const int be = ce / G;
+                double *pab = st + bidx(be, ce - be * G, beta, a.L) + 1;
                 if (a.det) *pab = *pab + tq * ve;
                 else red_add(pab, tq * ve);
             }
@@ -302,22 +327,21 @@ template <typename VT, int LOSS> static void *pick_b(int B, int G, bool rep)
     return G == 10 ? pick_bg<VT, LOSS, 10>(B, rep) : pick_bg<VT, LOSS, 0>(B, rep);
 }
 
-__global__ void k_batch_field(const double *state, int64_t p, int64_t nb, int G, int B, int beta, int field,
-                              double *out, int set, int64_t rpad)
+__global__ void k_batch_field(const double *state, int64_t p, const BLay L, int beta, int field, double *out, int set)
 {
-    const int S = B < BATCH_S ? B : BATCH_S;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
-        double *s = const_cast<double *>(state) + bidx(j, beta, nb, G, S, rpad) + field;
+        const int64_t b = j / L.G;
+        double *s = const_cast<double *>(state) + bidx(b, (int)(j - b * L.G), beta, L) + field;
         if (set) *s = out[j];
         else out[j] = *s;
     }
 }
 
 // fold the replicated x deltas of the hot blocks into the state (after a launch)
-__global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int hshift, int64_t nb, int G, int B,
-                             int64_t p, int64_t rpad, int64_t rstride)
+__global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int hshift, const BLay L, int B,
+                             int64_t p, int64_t rstride)
 {
-    const int S = B < BATCH_S ? B : BATCH_S;
+    const int G = L.G;
     const int64_t m = (int64_t)nrb * G * B;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
         const int beta = (int)(t % B);
@@ -329,14 +353,27 @@ __global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int
             sum += *r;
             *r = 0.0;
         }
-        const int64_t j = ((int64_t)rank << hshift) * G + q;
-        if (j < p) state[bidx(j, beta, nb, G, S, rpad)] += sum;
+        const int64_t b = (int64_t)rank << hshift;
+        if (b * G + q < p) state[bidx(b, q, beta, L)] += sum;
     }
 }
 
 }  // namespace ps
 
 using namespace ps;
+
+static BLay batch_layout(int64_t p, int G, int B, int hshift)
+{
+    BLay L{};
+    L.G = G;
+    L.S = B < BATCH_S ? B : BATCH_S;
+    L.body = ((p + G - 1) / G) * G * L.S * 2;
+    L.hstride = std::max<int64_t>(g_hstride, 2 * L.S);
+    L.nhot = g_hstride > 0 ? (g_nhot >= 0 ? g_nhot : (B >= 8 ? 128 : 32)) : 0;
+    L.hshift = std::max(0, std::min(hshift, 30));
+    L.region = L.body + (int64_t)L.nhot * G * L.hstride + g_rpad;
+    return L;
+}
 
 extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, const ps_params_t *prm,
                                 const double *lam2, int32_t B, double *state, double *alpha, const ps_sched_t *sched,
@@ -389,6 +426,7 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     a.nrb = nrb;
     a.hshift = std::max(0, (int)sched->hot_shift);
     a.rpad = g_rpad;
+    a.L = batch_layout(csr->n_cols, part->G, B, a.hshift);
     a.rstride = std::max<int64_t>(g_rstride, (int64_t)part->G * B);
     void *kern;
     const bool f64 = csr->value_type == PS_F64, sq = prm->loss == PS_LOSS_SQUARED;
@@ -416,7 +454,7 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     if (a.nrep > 0) {
         const int64_t m = (int64_t)nrb * G * B;
         k_batch_fold<<<(int)std::min<int64_t>((m + 255) / 256, 1024), 256, 0, (cudaStream_t)stream>>>(
-            state, xrep, a.nrep, nrb, a.hshift, a.nb, G, B, a.p, a.rpad, a.rstride);
+            state, xrep, a.nrep, nrb, a.hshift, a.L, B, a.p, a.rstride);
         CK(cudaGetLastError(), "ps_batch_run fold");
     }
     return PS_OK;
@@ -428,14 +466,13 @@ extern "C" int ps_batch_run(const ps_csr_t *csr, const ps_part_t *part, const ps
     return ps_batch_run_rep(csr, part, prm, lam2, B, state, alpha, sched, nullptr, 0, 0, stream);
 }
 
-extern "C" int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t beta, int32_t field, double *vec,
-                              int32_t set, void *stream)
+extern "C" int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t hot_shift, int32_t beta,
+                              int32_t field, double *vec, int32_t set, void *stream)
 {
     if (!state || !vec || beta < 0 || beta >= B || field < 0 || field > 1 || G < 1) return ps_fail(PS_EINVAL, "bad argument");
     if (p <= 0) return PS_OK;
-    const int64_t nb = (p + G - 1) / G;
-    k_batch_field<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(state, p, nb, G, B,
-                                                                                                  beta, field, vec, set, g_rpad);
+    k_batch_field<<<(int)std::min<int64_t>((p + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(
+        state, p, batch_layout(p, G, B, hot_shift), beta, field, vec, set);
     CK(cudaGetLastError(), "ps_batch_field launch");
     return PS_OK;
 }
@@ -448,12 +485,19 @@ extern "C" int ps_batch_tune(int64_t rpad, int64_t rstride)
     return PS_OK;
 }
 
+extern "C" int ps_batch_tune2(int32_t nhot, int64_t hstride)
+{
+    if (nhot < -1 || hstride < 0) return ps_fail(PS_EINVAL, "bad argument");
+    g_nhot = nhot;
+    g_hstride = hstride;
+    return PS_OK;
+}
+
 extern "C" int64_t ps_batch_state_doubles(int64_t p, int32_t G, int32_t B)
 {
     if (p < 0 || G < 1 || B < 1) return -1;
-    const int S = B < BATCH_S ? B : BATCH_S;
-    const int64_t nb = (p + G - 1) / G;
-    return (int64_t)(B / S) * (nb * G * S * 2 + g_rpad);
+    const BLay L = batch_layout(p, G, B, 0);
+    return (int64_t)(B / L.S) * L.region;
 }
 
 extern "C" int64_t ps_batch_rep_doubles(int32_t nrep, int32_t nrb, int32_t G, int32_t B)

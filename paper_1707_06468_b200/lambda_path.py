@@ -100,7 +100,7 @@ def _summary(dp, updates):
 
 def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epochs=30, seed=0,
                   mode="async", contention=4.0, device=None, keep_x=False, ctas=0, warps_per_cta=0, concurrent=1,
-                  flags=0, hot=None, batched=0):
+                  flags=0, hot=None, batched=0, nrep=None, nrb=None):
     """A ``solve(lam)`` closure over one DeviceProblem (uploaded once).
 
     ``concurrent`` > 1 (async mode): ``solve.batch(lams)`` runs that many
@@ -139,7 +139,7 @@ def device_solver(data, loss, partition, penalty_kind="group", step="1/2L", epoc
     solve.batch = None
     if batched > 0 and penalty_kind == "group" and samples is None:
         # lambda-batched kernel: `batched` states per launch share each sampled row
-        bp = BatchedPath(data, loss, partition, B=batched, device=device)
+        bp = BatchedPath(data, loss, partition, B=batched, device=device, nrep=nrep, nrb=nrb)
         bgamma = resolve_step_size(step, bp.dp.L, n, loss.lambda1 if loss.lambda1 > 0 else None)
 
         def batch(lams):
@@ -221,17 +221,20 @@ class BatchedPath:
     average is 12%, profiles/ncu_sps_r02.md).  ``field`` returns original
     coordinate order unless asked for the stored one.
 
-    ``nrep`` > 0 (default by B, AUTO_NREP): the x deltas of the ``nrb`` hottest
+    ``nrep`` > 0 (opt-in since the scattered hot-block layout): the x deltas of the ``nrb`` hottest
     blocks go to nrep replica accumulators (one per warp residue), folded into
     the state after each launch (ps_batch_run_rep).  With few states per row a
     hot block's x lines receive a RED from every row, and the per-line atomic
     rate caps the solve (~48 M rows/s at B = 2 whatever the grid)."""
 
-    # replicas (and replicated hottest blocks) of the x-delta accumulators by B
-    # (config 5, tools/gpu/exp_batch_rep.py: B = 2 / 4 / 8 +56% / +70% / +16%
-    # rows/s; at B = 16 the extra replica loads cost more than the spread REDs save)
-    AUTO_NREP = {1: 8, 2: 8, 4: 8, 8: 4, 16: 0}
-    AUTO_NRB = {1: 32, 2: 32, 4: 64, 8: 16, 16: 0}
+    # replicas of the x-delta accumulators: none by default since the scattered
+    # hot blocks of the state layout (csrc/batch.cu bidx: one coordinate sector per
+    # KB for the most frequent blocks) -- config 5 rows/s of one epoch with
+    # replicas / scattered: B = 2 79 / 115 M, B = 4 43 / 85 M, B = 8 25 / 63 M,
+    # B = 16 (no replicas) 25 / 40 M (tools/gpu/exp_batch_scatter.py); replicas on
+    # top of the scattered layout cost 20-60%.  nrep / nrb keep the option.
+    AUTO_NREP = {1: 0, 2: 0, 4: 0, 8: 0, 16: 0}
+    AUTO_NRB = {1: 0, 2: 0, 4: 0, 8: 0, 16: 0}
 
     def __init__(self, data, loss, partition, B=16, device=None, dp=None, spread=True, nrep=None, nrb=None):
         from . import _lib
@@ -313,7 +316,7 @@ class BatchedPath:
         with self.torch.cuda.device(self.dp.device):
             out = self.torch.empty(self.dp.p_dev, dtype=self.torch.float64, device=self.dp.device)
             _lib.check(_lib.load().ps_batch_field(self.state.data_ptr(), self.dp.p_dev, int(self.dp.part.G), self.B,
-                                                  int(beta), int(f), out.data_ptr(), 0, _lib.stream_ptr()))
+                                                  int(self.dp.hot_shift), int(beta), int(f), out.data_ptr(), 0, _lib.stream_ptr()))
             if original and self._perm_long is not None:
                 out = out[self._perm_long]
         return out

@@ -50,11 +50,14 @@ def test_batched_deterministic_replay_matches_single_lambda(cuda, B, small_cases
             assert _rel(x, g["grp_contig__x"][0]) <= 1e-9
 
 
-@pytest.mark.parametrize("B,factors", [(8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005)), (2, (0.3, 0.01))],
-                         ids=["B8", "B2"])
-def test_batched_async_reaches_each_optimum(cuda, B, factors):
-    """Spread block layout; the hottest blocks commit their x deltas
-    through replicated accumulators (ps_batch_run_rep, folded after the launch)."""
+@pytest.mark.parametrize("B,factors,nrep", [(8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005), 0), (2, (0.3, 0.01), 0),
+                                            (16, (0.5, 0.01), 0), (8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005), 4),
+                                            (2, (0.3, 0.01), 8)],
+                         ids=["B8", "B2", "B16", "B8rep", "B2rep"])
+def test_batched_async_reaches_each_optimum(cuda, B, factors, nrep):
+    """Spread block layout with the scattered hot blocks of the state (the
+    default: no replicas), and the opt-in replicated x-delta accumulators of the
+    hottest blocks (ps_batch_run_rep, folded after the launch)."""
     rng = np.random.default_rng(11)
     data = problems._zipf_logistic(rng, 8000, 40000, 20, 1.1, 100)
     part = pb.contiguous_partition(data.n_features, 10)
@@ -62,11 +65,11 @@ def test_batched_async_reaches_each_optimum(cuda, B, factors):
     loss = pb.Loss("logistic", lam1)
     lmax = pb.group_lambda_max(data, part)
     lams = [f * lmax for f in factors]
-    solve = device_solver(data, loss, part, epochs=60, seed=3, batched=B)
+    solve = device_solver(data, loss, part, epochs=60, seed=3, batched=B, nrep=nrep, nrb=16 if nrep else 0)
     res = solve.batch(lams)
     bp = solve.batched
     assert bp.dp.perm is not None  # spread layout
-    assert bp.nrep == BatchedPath.AUTO_NREP[B] > 0  # replicated hottest blocks at both B
+    assert bp.nrep == nrep and BatchedPath.AUTO_NREP[B] == 0
     n = data.n_samples
     for beta, (lam, r) in enumerate(zip(lams, res)):
         dp = DeviceProblem(data, loss, pb.GroupL2Penalty(lam), part, drop_dead_blocks=True, hot_max=0)
