@@ -62,7 +62,10 @@ struct BArgs {
     BLay L;                 // state layout (bidx)
 };
 
-constexpr int BATCH_T = 512;       // threads per CTA (16 warps)
+#ifndef BATCH_THREADS
+#define BATCH_THREADS 512
+#endif
+constexpr int BATCH_T = BATCH_THREADS;  // threads per CTA (16 warps; A/B knob)
 // A/B knob: -DBATCH_MINB=2 caps the kernel at 64 registers (two CTAs per SM)
 #ifdef BATCH_MINB
 #define BATCH_BOUNDS __launch_bounds__(BATCH_T, BATCH_MINB)
