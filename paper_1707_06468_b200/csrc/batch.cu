@@ -106,6 +106,17 @@ __host__ __device__ __forceinline__ int64_t bidx(int64_t b, int q, int beta, con
     if (r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0) return base + L.body + (r * L.G + q) * L.hstride;
     return base + (b * L.G + q) * L.S * 2;
 }
+// the same address split for the kernel's block loops: coordinate q of stored
+// block b in this lane's state lives at lane_base + off + q * qs, with
+// lane_base = bidx(0, 0, beta) fixed per lane -- one hot test per block
+// instead of one per coordinate access
+__device__ __forceinline__ void bref(int64_t b, const BLay &L, int64_t &off, int &qs)
+{
+    const int64_t r = b >> L.hshift;
+    const bool hot = r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0;
+    off = hot ? L.body + r * (L.G * L.hstride) : b * (L.G * L.S * 2);
+    qs = hot ? (int)L.hstride : L.S * 2;
+}
 // layout knobs (doubles): the region pad and the stride of one (replica, hot
 // block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
 static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
@@ -140,7 +151,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
     double *sa = smem_dyn + (size_t)wib * BATCH_SM_WARP + 32;  // [rank][16]
     const int G = GT > 0 ? GT : a.G;
     const int64_t p = a.p;
-    double *const st = a.state;
+    double *const st = a.state + ((int64_t)(beta / a.L.S) * a.L.region + (beta % a.L.S) * 2);  // this lane's state (region, slot)
     const double lam2 = a.lam2[beta];
     const VT *valp = reinterpret_cast<const VT *>(a.val);
     const VT *yp = reinterpret_cast<const VT *>(a.y);
@@ -177,7 +188,10 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const int e = sub + LPB * j;
             const int ce = __shfl_sync(FULL, col, e & 31);
             const int be = ce / G;
-            xm[j] = (e < k) ? ld_cg(st + bidx(be, ce - be * G, beta, a.L)) : 0.0;
+            int64_t mo;
+            int mq;
+            bref(be, a.L, mo, mq);
+            xm[j] = (e < k) ? ld_cg(st + mo + (ce - be * G) * mq) : 0.0;
             const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
             if (rk >= 0)
                 for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
@@ -220,22 +234,25 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         // ---- every block of T_i, all B states; the next block's state loads
         // are issued before the current block is computed
         double2 cur[RMAX];
-        auto load_blk = [&](int tb, double2 *v) {
+        auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs) {
             const int b = sblk[tb];
             const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
             const int rk = rep_rank<REP>(a, b);
+            bref(b, a.L, off, qs);
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
-                v[r] = q < nq ? ld_cg2(st + bidx(b, q, beta, a.L)) : make_double2(0.0, 0.0);
+                v[r] = q < nq ? ld_cg2(st + off + q * qs) : make_double2(0.0, 0.0);
                 if (rk >= 0 && q < nq)
                     for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
         };
-        if (g > 0) load_blk(0, cur);
+        int64_t coff = 0, noff = 0;
+        int cqs = 0, nqs = 0;
+        if (g > 0) load_blk(0, cur, coff, cqs);
         for (int tb = 0; tb < g; tb++) {
             double2 nxt[RMAX];
-            if (tb + 1 < g) load_blk(tb + 1, nxt);
+            if (tb + 1 < g) load_blk(tb + 1, nxt, noff, nqs);
             const int b = sblk[tb];
             const double d = __shfl_sync(FULL, dB, tb);
             const double kd = a.kappa * d;
@@ -269,7 +286,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                 for (int r = 0; r < RMAX; r++) {
                     const int q = sub + LPB * r;
                     if (q < nq) {
-                        double *px = st + bidx(b, q, beta, a.L);
+                        double *px = st + coff + q * cqs;
                         const double z = u[r] * f;
                         if (a.det) {
                             *px = cur[r].x + (z - cur[r].x);
@@ -285,6 +302,8 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             }
 #pragma unroll
             for (int r = 0; r < RMAX; r++) cur[r] = nxt[r];
+            coff = noff;
+            cqs = nqs;
         }
         // ---- abar on S_i: ((new - replaced)/n) a_i
         rep = __shfl_sync(FULL, rep, beta);
@@ -295,7 +314,10 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const double ve = __shfl_sync(FULL, val, e & 31);
             if (e < k) {
                 const int be = ce / G;
-                double *pab = st + bidx(be, ce - be * G, beta, a.L) + 1;
+                int64_t ao;
+                int aq;
+                bref(be, a.L, ao, aq);
+                double *pab = st + ao + (ce - be * G) * aq + 1;
                 if (a.det) *pab = *pab + tq * ve;
                 else red_add(pab, tq * ve);
             }
