@@ -178,6 +178,15 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             col = __ldg(a.col + lo + lane);
             val = widen(__ldg(valp + lo + lane));
         }
+        // this lane's nonzero: the offset of x[col] from any lane's state base (one
+        // layout lookup per nonzero; the margin loads and the abar REDs take it by shuffle)
+        int64_t eoff = 0;
+        if (col >= 0) {
+            const int be = col / G;
+            int eqs;
+            bref(be, a.L, eoff, eqs);
+            eoff += (col - be * G) * eqs;
+        }
         const double yb = widen(__ldg(yp + i));
         double old = 0.0;  // alpha_i of this lane's state (lanes < B)
         if (sub == 0) old = a.det ? a.alpha[i * B + beta] : ld_cg(a.alpha + i * B + beta);
@@ -186,15 +195,14 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
 #pragma unroll
         for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
             const int e = sub + LPB * j;
-            const int ce = __shfl_sync(FULL, col, e & 31);
-            const int be = ce / G;
-            int64_t mo;
-            int mq;
-            bref(be, a.L, mo, mq);
-            xm[j] = (e < k) ? ld_cg(st + mo + (ce - be * G) * mq) : 0.0;
-            const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
-            if (rk >= 0)
-                for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
+            const int64_t mo = __shfl_sync(FULL, eoff, e & 31);
+            xm[j] = (e < k) ? ld_cg(st + mo) : 0.0;
+            if (REP) {
+                const int ce = __shfl_sync(FULL, col, e & 31);
+                const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
+                if (rk >= 0)
+                    for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
+            }
         }
         const int blk = col >= 0 ? col / G : -1 - lane;
         const unsigned peers = __match_any_sync(FULL, blk);
@@ -233,7 +241,6 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         }
         // ---- every block of T_i, all B states; the next block's state loads
         // are issued before the current block is computed
-        double2 cur[RMAX];
         auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs) {
             const int b = sblk[tb];
             const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
@@ -247,12 +254,8 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                     for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
         };
-        int64_t coff = 0, noff = 0;
-        int cqs = 0, nqs = 0;
-        if (g > 0) load_blk(0, cur, coff, cqs);
-        for (int tb = 0; tb < g; tb++) {
-            double2 nxt[RMAX];
-            if (tb + 1 < g) load_blk(tb + 1, nxt, noff, nqs);
+        // two buffers in turn (no register copies between blocks)
+        auto process = [&](int tb, const double2 *cur, const int64_t coff, const int cqs) {
             const int b = sblk[tb];
             const double d = __shfl_sync(FULL, dB, tb);
             const double kd = a.kappa * d;
@@ -277,7 +280,10 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                 ss += __shfl_xor_sync(FULL, ss, o);
                 zero = (__shfl_xor_sync(FULL, (int)zero, o) != 0) && zero;
             }
-            const double f = group_factor(sqrt(ss), gB * d, lam2);
+            // deterministic mode: penalties.py:103-108's arithmetic (sqrt, divide); asynchronous:
+            // one reciprocal square root (the objective-level parity of the async kernels)
+            const double f = a.det ? group_factor(sqrt(ss), gB * d, lam2)
+                                   : (ss > 0.0 ? fmax(0.0, __fma_rn(-(gB * d * lam2), rsqrt(ss), 1.0)) : 0.0);
             // zero block kept at zero: delta 0, nothing committed (the lane
             // kernel's skip); a zeroed block is stored (zero commits)
             if (!(f == 0.0 && zero && a.skip_zero)) {
@@ -300,24 +306,28 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                     }
                 }
             }
-#pragma unroll
-            for (int r = 0; r < RMAX; r++) cur[r] = nxt[r];
-            coff = noff;
-            cqs = nqs;
+        };
+        double2 bufa[RMAX], bufb[RMAX];
+        int64_t aoff = 0, boff = 0;
+        int aqs = 0, bqs = 0;
+        if (g > 0) load_blk(0, bufa, aoff, aqs);
+        for (int tb = 0; tb < g; tb += 2) {
+            if (tb + 1 < g) load_blk(tb + 1, bufb, boff, bqs);
+            process(tb, bufa, aoff, aqs);
+            if (tb + 1 < g) {
+                if (tb + 2 < g) load_blk(tb + 2, bufa, aoff, aqs);
+                process(tb + 1, bufb, boff, bqs);
+            }
         }
         // ---- abar on S_i: ((new - replaced)/n) a_i
         rep = __shfl_sync(FULL, rep, beta);
         const double tq = (nw - rep) / a.n_d;  // saga.py:182-184: (delta / n) * vals
         for (int e0 = 0; e0 < k; e0 += LPB) {
             const int e = e0 + sub;
-            const int ce = __shfl_sync(FULL, col, e & 31);
+            const int64_t ao = __shfl_sync(FULL, eoff, e & 31);
             const double ve = __shfl_sync(FULL, val, e & 31);
             if (e < k) {
-                const int be = ce / G;
-                int64_t ao;
-                int aq;
-                bref(be, a.L, ao, aq);
-                double *pab = st + ao + (ce - be * G) * aq + 1;
+                double *pab = st + ao + 1;
                 if (a.det) *pab = *pab + tq * ve;
                 else red_add(pab, tq * ve);
             }
