@@ -190,20 +190,6 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         const double yb = widen(__ldg(yp + i));
         double old = 0.0;  // alpha_i of this lane's state (lanes < B)
         if (sub == 0) old = a.det ? a.alpha[i * B + beta] : ld_cg(a.alpha + i * B + beta);
-        // margin loads issued first: x[col_e][beta] for this lane's nonzeros e = sub + LPB j
-        double xm[(32 + LPB - 1) / LPB];
-#pragma unroll
-        for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
-            const int e = sub + LPB * j;
-            const int64_t mo = __shfl_sync(FULL, eoff, e & 31);
-            xm[j] = (e < k) ? ld_cg(st + mo) : 0.0;
-            if (REP) {
-                const int ce = __shfl_sync(FULL, col, e & 31);
-                const int rk = (e < k) ? rep_rank<REP>(a, ce / G) : -1;
-                if (rk >= 0)
-                    for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
-            }
-        }
         const int blk = col >= 0 ? col / G : -1 - lane;
         const unsigned peers = __match_any_sync(FULL, blk);
         const int lead = __ffs(peers) - 1;
@@ -217,6 +203,43 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             if (lead == lane) sblk[rank] = blk;
         }
         __syncwarp();
+        auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs) {
+            const int b = sblk[tb];
+            const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
+            const int rk = rep_rank<REP>(a, b);
+            bref(b, a.L, off, qs);
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) {
+                const int q = sub + LPB * r;
+                v[r] = q < nq ? ld_cg2(st + off + q * qs) : make_double2(0.0, 0.0);
+                if (rk >= 0 && q < nq)
+                    for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
+            }
+        };
+        // the first block of T_i (the hottest one present: the smallest stored index) is
+        // loaded once, ahead of the margin: its x values feed the margin AND the block
+        // update below, so the hottest lines take one load per row instead of two
+        // (sps_step gathers x_hat once, saga.py:169-172)
+        double2 bufa[RMAX], bufb[RMAX];
+        int64_t aoff = 0, boff = 0;
+        int aqs = 0, bqs = 0;
+        if (g > 0) load_blk(0, bufa, aoff, aqs);
+        const unsigned first0 = __ballot_sync(FULL, col >= 0 && rank == 0);  // nonzeros in that block
+        // margin loads: x[col_e][beta] for this lane's other nonzeros e = sub + LPB j
+        double xm[(32 + LPB - 1) / LPB];
+#pragma unroll
+        for (int j = 0; j < (32 + LPB - 1) / LPB; j++) {
+            const int e = sub + LPB * j;
+            const int64_t mo = __shfl_sync(FULL, eoff, e & 31);
+            const bool need = e < k && !((first0 >> (e & 31)) & 1u);
+            xm[j] = need ? ld_cg(st + mo) : 0.0;
+            if (REP) {
+                const int ce = __shfl_sync(FULL, col, e & 31);
+                const int rk = need ? rep_rank<REP>(a, ce / G) : -1;
+                if (rk >= 0)
+                    for (int rr = 0; rr < a.nrep; rr++) xm[j] += ld_cg(rep_ptr(a, rr, rk, ce - (ce / G) * G, beta, B, G));
+            }
+        }
         // block weights of T_i: lane t holds d_B of rank t
         double dB = 0.0;
         if (lane < g) dB = __ldg(a.bd + sblk[lane]);
@@ -227,6 +250,13 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const int e = sub + LPB * j;
             const double ve = __shfl_sync(FULL, val, e & 31);
             part = __fma_rn(ve, xm[j], part);  // xm = 0 past the row
+        }
+        if (g > 0) {  // the first block's nonzeros, from its loaded coordinates (sa = 0 where the row has none)
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) {
+                const int q = sub + LPB * r;
+                if (q < G) part = __fma_rn(sa[q], bufa[r].x, part);
+            }
         }
 #pragma unroll
         for (int o = B; o < 32; o <<= 1) part += __shfl_xor_sync(FULL, part, o);
@@ -241,19 +271,6 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         }
         // ---- every block of T_i, all B states; the next block's state loads
         // are issued before the current block is computed
-        auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs) {
-            const int b = sblk[tb];
-            const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
-            const int rk = rep_rank<REP>(a, b);
-            bref(b, a.L, off, qs);
-#pragma unroll
-            for (int r = 0; r < RMAX; r++) {
-                const int q = sub + LPB * r;
-                v[r] = q < nq ? ld_cg2(st + off + q * qs) : make_double2(0.0, 0.0);
-                if (rk >= 0 && q < nq)
-                    for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
-            }
-        };
         // two buffers in turn (no register copies between blocks)
         auto process = [&](int tb, const double2 *cur, const int64_t coff, const int cqs) {
             const int b = sblk[tb];
@@ -307,11 +324,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
                 }
             }
         };
-        double2 bufa[RMAX], bufb[RMAX];
-        int64_t aoff = 0, boff = 0;
-        int aqs = 0, bqs = 0;
-        if (g > 0) load_blk(0, bufa, aoff, aqs);
-        for (int tb = 0; tb < g; tb += 2) {
+        for (int tb = 0; tb < g; tb += 2) {  // block 0 is in bufa already
             if (tb + 1 < g) load_blk(tb + 1, bufb, boff, bqs);
             process(tb, bufa, aoff, aqs);
             if (tb + 1 < g) {
