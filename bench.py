@@ -542,9 +542,8 @@ def lambda_path_ttt(cfg, lams, mine, epochs, with_oracle=True):
             t += s.elapsed_time(e) / 1e3
             its.append((ep + 1) * n)
             secs.append(t)
-            for j, k in enumerate(mine):
-                f = bp.summary(j, 0)["objective"]
-                rels[j].append(max((f - stars[k]["fstar"]) / abs(stars[k]["fstar"]), 1e-300))
+            for j, (k, sm) in enumerate(zip(mine, bp.summaries(range(len(mine)), 0))):
+                rels[j].append(max((sm["objective"] - stars[k]["fstar"]) / abs(stars[k]["fstar"]), 1e-300))
         for j, rec in enumerate(out):
             # from the first epoch mark on (x0 = 0 is itself optimal at lambda_max), as the solve-alone record
             hit = _first_crossing(its[1:], secs[1:], rels[j][1:], n, 1e-6)
