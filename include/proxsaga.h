@@ -250,8 +250,10 @@ int ps_batch_tune(int64_t rpad, int64_t rstride);
  * region's hot area at (rank*G + q)*hstride doubles, one sector per hstride (defaults: 128 blocks
  * from B = 8 and 32 below (nhot = -1), 128 doubles = 1 KB; nhot = 0 or hstride = 0: every block in
  * the contiguous record).
+ * hshare: a warp loads stored block 0 from L2 on every hshare-th of its rows and reads the CTA's
+ * shared copy of it on the others (default 4; 0 = every row).
  * Process-wide; allocate states after setting */
-int ps_batch_tune2(int32_t nhot, int64_t hstride);
+int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare);
 /* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state);
  * hot_shift = the ps_sched_t.hot_shift the state is run with (it places the scattered hot blocks) */
 int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t hot_shift, int32_t beta, int32_t field,

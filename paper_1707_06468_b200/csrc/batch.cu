@@ -60,6 +60,7 @@ struct BArgs {
     int32_t nrep, nrb, hshift;
     int64_t rpad, rstride;  // state region pad; doubles per (replica, hot block) chunk
     BLay L;                 // state layout (bidx)
+    int32_t hshare;         // > 0: the CTA shares its loads of stored block 0 (see the kernel)
 };
 
 #ifndef BATCH_THREADS
@@ -86,6 +87,7 @@ constexpr int BATCH_T = BATCH_THREADS;  // threads per CTA (16 warps; A/B knob)
 constexpr int BATCH_S = 2;
 constexpr int PROGRESS_BATCH_B = 16;           // rows per progress bump of a warp
 constexpr int BATCH_SM_WARP = 32 + 32 * 16;    // per-warp shared doubles: block ids + row values [32][16]
+constexpr int BATCH_SM_SHARE = 32 * 8 * 2;     // per-CTA shared doubles: stored block 0's (x, abar) per (lane, r)
 // Region g of the state is [body | hot area | pad]: body = nb*G*S*2 doubles in
 // [block][q][S](x, abar) order.  SCATTERED HOT BLOCKS: stored block b with
 // (b & ((1 << hshift) - 1)) == 0 and rank r = b >> hshift < nhot (the most
@@ -121,6 +123,7 @@ __device__ __forceinline__ void bref(int64_t b, const BLay &L, int64_t &off, int
 // block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
 static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
 static int64_t g_hstride = 128;  // scattered hot blocks: one sector per KB (adjacent lines measured slower below B = 16)
+static int32_t g_hshare = 4;     // rows between a warp's own L2 loads of stored block 0 (0: every row); ps_batch_tune2
 static int32_t g_nhot = -1;      // how many: -1 = by B (128 from B = 8, else 32: tools/gpu/exp_batch_scatter.py); ps_batch_tune2
 
 // rank of a replicated hot block, or -1
@@ -153,6 +156,31 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
     const int64_t p = a.p;
     double *const st = a.state + ((int64_t)(beta / a.L.S) * a.L.region + (beta % a.L.S) * 2);  // this lane's state (region, slot)
     const double lam2 = a.lam2[beta];
+    // CTA-shared loads of stored block 0 (the most frequent block: in ~every row of a
+    // Zipf-headed problem): every warp needs its G x B (x, abar) pairs at the start of
+    // every row, and those loads queue behind everyone's REDs on the same lines.  Each
+    // warp loads them from L2 on every hshare-th row only (staggered by warp) and
+    // publishes them here; on its other rows it reads this copy, which another warp of
+    // the CTA refreshed a fraction of a row time ago -- an inconsistent read like any
+    // other here (the row takes ~16 block updates to commit, with thousands of rows in
+    // flight).  Nothing is write-combined: every delta still goes to L2 at once, so
+    // abar stays the exact average and the certified gaps are unchanged (K3b).
+    double2 *const hs = reinterpret_cast<double2 *>(smem_dyn + (size_t)nwib * BATCH_SM_WARP) + lane * RMAX;
+    const bool share = !REP && !a.det && a.hshare > 0 && a.nb > 1;
+    if (share) {
+        if (wib == 0) {
+            int64_t o0;
+            int q0;
+            bref(0, a.L, o0, q0);
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) {
+                const int q = sub + LPB * r;
+                hs[r] = q < G ? ld_cg2(st + o0 + q * q0)
+                              : make_double2(0.0, 0.0);
+            }
+        }
+        __syncthreads();
+    }
     const VT *valp = reinterpret_cast<const VT *>(a.val);
     const VT *yp = reinterpret_cast<const VT *>(a.y);
 
@@ -223,7 +251,14 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         double2 bufa[RMAX], bufb[RMAX];
         int64_t aoff = 0, boff = 0;
         int aqs = 0, bqs = 0;
-        if (g > 0) load_blk(0, bufa, aoff, aqs);
+        const bool hot0 = share && g > 0 && sblk[0] == 0;
+        const bool fresh = !hot0 || (done + wib) % a.hshare == 0;
+        if (g > 0 && fresh) load_blk(0, bufa, aoff, aqs);
+        if (hot0 && !fresh) {
+            bref(0, a.L, aoff, aqs);
+#pragma unroll
+            for (int r = 0; r < RMAX; r++) bufa[r] = hs[r];
+        }
         const unsigned first0 = __ballot_sync(FULL, col >= 0 && rank == 0);  // nonzeros in that block
         // margin loads: x[col_e][beta] for this lane's other nonzeros e = sub + LPB j
         double xm[(32 + LPB - 1) / LPB];
@@ -256,6 +291,10 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
                 if (q < G) part = __fma_rn(sa[q], bufa[r].x, part);
+            }
+            if (hot0 && fresh) {  // publish this warp's load of stored block 0
+#pragma unroll
+                for (int r = 0; r < RMAX; r++) hs[r] = bufa[r];
             }
         }
 #pragma unroll
@@ -475,6 +514,7 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     a.hshift = std::max(0, (int)sched->hot_shift);
     a.rpad = g_rpad;
     a.L = batch_layout(csr->n_cols, part->G, B, a.hshift);
+    a.hshare = g_hshare;
     a.rstride = std::max<int64_t>(g_rstride, (int64_t)part->G * B);
     void *kern;
     const bool f64 = csr->value_type == PS_F64, sq = prm->loss == PS_LOSS_SQUARED;
@@ -483,7 +523,7 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     if (f64) kern = sq ? pick_b<double, PS_LOSS_SQUARED>(B, G, rep) : pick_b<double, PS_LOSS_LOGISTIC>(B, G, rep);
     else kern = sq ? pick_b<float, PS_LOSS_SQUARED>(B, G, rep) : pick_b<float, PS_LOSS_LOGISTIC>(B, G, rep);
     const int wpc = sched->warps_per_cta > 0 ? std::min(sched->warps_per_cta, BATCH_T / 32) : BATCH_T / 32;
-    const size_t smem = (size_t)wpc * BATCH_SM_WARP * 8;
+    const size_t smem = ((size_t)wpc * BATCH_SM_WARP + BATCH_SM_SHARE) * 8;
     if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "ps_batch_run smem attribute");
     int dev = 0, sms = 148, per_sm = 1;
@@ -533,11 +573,12 @@ extern "C" int ps_batch_tune(int64_t rpad, int64_t rstride)
     return PS_OK;
 }
 
-extern "C" int ps_batch_tune2(int32_t nhot, int64_t hstride)
+extern "C" int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare)
 {
-    if (nhot < -1 || hstride < 0) return ps_fail(PS_EINVAL, "bad argument");
+    if (nhot < -1 || hstride < 0 || hshare < 0) return ps_fail(PS_EINVAL, "bad argument");
     g_nhot = nhot;
     g_hstride = hstride;
+    g_hshare = hshare;
     return PS_OK;
 }
 
