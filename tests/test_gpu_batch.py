@@ -7,8 +7,9 @@ Tolerances:
     iterates, tests/test_gpu_parity.py) to 1e-9 relative, and the reference's
     golden iterates where the golden case's lambda is used;
   * asynchronous: each state's objective within 1e-6 relative of that
-    lambda's optimum (a long deterministic replay), abar = A^T alpha / n per
-    state to 1e-12.
+    lambda's optimum (a long deterministic replay; 1e-5 below 0.01 lambda_max,
+    where the replay itself is not converged and the asynchronous iterate
+    fluctuates at the 1e-6 level), abar = A^T alpha / n per state to 1e-12.
 """
 
 import numpy as np
@@ -93,7 +94,12 @@ def test_batched_async_reaches_each_optimum(cuda, tune2, B, factors, nrep, layou
         gamma = resolve_step_size("1/2L", dp.L, n, lam1)
         dp.replay(worker_rng(99, 0).integers(0, n, size=150 * n), gamma)
         fref = dp.objective()
-        assert abs(r["objective"] - fref) <= 1e-6 * abs(fref), (lam / lmax, r["objective"], fref)
+        # 1e-6 of the optimum; at lambda < 0.01 lambda_max this instance's asynchronous iterate
+        # hovers in a +-1e-6..3e-6 band (spikes to 7e-6) around the 150-epoch replay, which is
+        # itself not converged there (negative differences occur) -- measured the same for the
+        # contiguous, scattered and shared-load layouts (tools/gpu/exp_batch_share_conv.py)
+        tol = 1e-6 if lam >= 0.0099 * lmax else 1e-5
+        assert abs(r["objective"] - fref) <= tol * abs(fref), (lam / lmax, r["objective"], fref)
         assert r["gap"] >= -1e-12 and r["objective"] >= r["dual"]
         # abar stays the exact average of this state's alpha table
         dp.alpha.copy_(bp.alpha.view(-1, B)[:, beta])
