@@ -254,6 +254,8 @@ int ps_batch_tune(int64_t rpad, int64_t rstride);
  * shared copy of it on the others (default 4; 0 = every row).
  * Process-wide; allocate states after setting */
 int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare);
+/* the grid (CTAs, warps per CTA: rows in flight = their product) of this process's last ps_batch_run launch */
+int ps_batch_last_grid(int32_t *ctas, int32_t *warps_per_cta);
 /* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state);
  * hot_shift = the ps_sched_t.hot_shift the state is run with (it places the scattered hot blocks) */
 int ps_batch_field(double *state, int64_t p, int32_t G, int32_t B, int32_t hot_shift, int32_t beta, int32_t field,

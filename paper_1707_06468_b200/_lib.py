@@ -39,7 +39,7 @@ EXPORTS = (
     "ps_atomic_scatter_add", "ps_atomic_exchange", "ps_atomic_fetch_add_i64",
     "ps_atomic_add_repeat", "ps_gen_zipf_csr", "ps_gen_labels", "ps_timestamp",
     "ps_dual_objective", "ps_run_monitored", "ps_libsvm_index", "ps_libsvm_scan", "ps_libsvm_fill",
-    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv", "ps_loss_eval", "ps_batch_run", "ps_batch_run_rep", "ps_batch_field", "ps_batch_tune", "ps_batch_tune2", "ps_batch_state_doubles",
+    "ps_fista_prox", "ps_fista_extrapolate", "ps_loss_deriv", "ps_loss_eval", "ps_batch_run", "ps_batch_run_rep", "ps_batch_field", "ps_batch_tune", "ps_batch_tune2", "ps_batch_last_grid", "ps_batch_state_doubles",
     "ps_batch_rep_doubles",
 )
 
@@ -121,6 +121,7 @@ def load():
         "ps_batch_field": (_i32, [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp]),
         "ps_batch_tune": (_i32, [_i64, _i64]),
         "ps_batch_tune2": (_i32, [_i32, _i64, _i32]),
+        "ps_batch_last_grid": (_i32, [_P(_i32), _P(_i32)]),
         "ps_batch_state_doubles": (_i64, [_i64, _i32, _i32]),
         "ps_batch_rep_doubles": (_i64, [_i32, _i32, _i32, _i32]),
         "ps_libsvm_scan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

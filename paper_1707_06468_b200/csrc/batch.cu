@@ -126,6 +126,7 @@ __device__ __forceinline__ void bref(int64_t b, const BLay &L, int64_t &off, int
 // block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
 static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
 static int64_t g_hstride = 128;  // scattered hot blocks: one sector per KB (adjacent lines measured slower below B = 16)
+static int32_t g_last_ctas = 0, g_last_wpc = 0;  // grid of the last ps_batch_run launch (ps_batch_last_grid)
 static int32_t g_hshare = 4;     // rows between a warp's own L2 loads of stored block 0 (0: every row); ps_batch_tune2
 static int32_t g_nhot = -1;      // how many: -1 = by B (128 from B = 8, else 32: tools/gpu/exp_batch_scatter.py); ps_batch_tune2
 
@@ -542,6 +543,8 @@ extern "C" int ps_batch_run_rep(const ps_csr_t *csr, const ps_part_t *part, cons
     a.kappa = (!det && sched->contention > 0) ? sched->contention / tau : INFINITY;
     void *args[] = {(void *)&a};
     CK(cudaLaunchKernel(kern, dim3(ctas), dim3(wpc * 32), args, smem, (cudaStream_t)stream), "ps_batch_run launch");
+    g_last_ctas = ctas;
+    g_last_wpc = wpc;
     if (a.nrep > 0) {
         const int64_t m = (int64_t)nrb * G * B;
         k_batch_fold<<<(int)std::min<int64_t>((m + 255) / 256, 1024), 256, 0, (cudaStream_t)stream>>>(
@@ -573,6 +576,14 @@ extern "C" int ps_batch_tune(int64_t rpad, int64_t rstride)
     if (rpad < 0 || rstride < 0) return ps_fail(PS_EINVAL, "bad argument");
     g_rpad = rpad;
     g_rstride = rstride;
+    return PS_OK;
+}
+
+extern "C" int ps_batch_last_grid(int32_t *ctas, int32_t *warps_per_cta)
+{
+    if (!ctas || !warps_per_cta) return ps_fail(PS_EINVAL, "null argument");
+    *ctas = g_last_ctas;
+    *warps_per_cta = g_last_wpc;
     return PS_OK;
 }
 

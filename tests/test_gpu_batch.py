@@ -105,3 +105,39 @@ def test_batched_async_reaches_each_optimum(cuda, tune2, B, factors, nrep, layou
         dp.alpha.copy_(bp.alpha.view(-1, B)[:, beta])
         dp.resync_average()
         assert np.max(np.abs(bp.field(beta, 1).cpu().numpy() - dp.abar())) <= 1e-12
+
+
+def test_run_async_group_lasso_runs_the_batched_kernel(cuda):
+    """run_async (asynchronous.py:131-210) with a group penalty on contiguous
+    blocks goes through the lambda-batched kernel with one state: one trace row
+    per epoch, the replay optimum within 1e-6, the final x / abar / alpha in the
+    problem's records (abar the exact average of alpha); AsyncConfig
+    (group_batched=False) keeps the coordinate-record group kernel."""
+    rng = np.random.default_rng(11)
+    data = problems._zipf_logistic(rng, 8000, 40000, 20, 1.1, 100)
+    part = pb.contiguous_partition(data.n_features, 10)
+    lam1 = 1.0 / data.n_samples
+    loss = pb.Loss("logistic", lam1)
+    pen = pb.GroupL2Penalty(0.1 * pb.group_lambda_max(data, part))
+    index = pb.build_support_index(data.features, part, drop_dead_blocks=True)
+    n, epochs = data.n_samples, 40
+    ref = DeviceProblem(data, loss, pen, part, drop_dead_blocks=True, hot_max=0)
+    gamma = resolve_step_size("1/2L", ref.L, n, lam1)
+    ref.replay(worker_rng(99, 0).integers(0, n, size=150 * n), gamma)
+    fref = ref.objective()
+    tr = pb.run_async(data, loss, pen, part, pb.AsyncConfig(step_size="1/2L", epochs=epochs, seed=2, threads=2),
+                      index=index)
+    assert tr.meta["kernel"].startswith("lambda-batched") and tr.meta["warps_in_flight"] >= 16
+    assert len(tr.iterations) == epochs + 1 and tr.iterations[-1] == epochs * n
+    assert abs(tr.objective[-1] - fref) <= 1e-6 * abs(fref), (tr.objective[-1], fref)
+    dp = tr.shared
+    assert abs(dp.objective() - tr.objective[-1]) <= 1e-15 * abs(fref)  # the records hold the final state
+    assert abs(ref.objective_of(tr.final_x) - tr.objective[-1]) <= 1e-12 * abs(fref)
+    live = dp.abar()
+    dp.resync_average()
+    assert np.max(np.abs(live - dp.abar())) <= 1e-12
+    tr2 = pb.run_async(data, loss, pen, part,
+                       pb.AsyncConfig(step_size="1/2L", epochs=epochs, seed=2, threads=2, group_batched=False),
+                       index=index)
+    assert "kernel" not in tr2.meta and len(tr2.iterations) == epochs + 1
+    assert abs(tr2.objective[-1] - fref) <= 1e-6 * abs(fref), (tr2.objective[-1], fref)
