@@ -244,8 +244,10 @@ class BatchedPath:
             raise ValueError("B must be 1, 2, 4, 8 or 16")
         self.dp = dp if dp is not None else DeviceProblem(data, loss, GroupL2Penalty(0.0), partition, device=device,
                                                           drop_dead_blocks=True, hot_max=None if spread else 0)
-        if self.dp.perm is not None and self.dp.part_kind != "contiguous":
-            raise ValueError("the batched path needs a contiguous partition")
+        if self.dp.part_kind != "contiguous" or not 1 <= int(self.dp.part.G) <= 16:
+            raise ValueError("the batched path needs a contiguous partition with blocks of <= 16 coordinates")
+        if int(self.dp.part.max_row_nnz) > 32 or self.dp.row_ptr_type != 0:
+            raise ValueError("the batched path needs rows of <= 32 nonzeros and int32 row pointers")
         torch = self.torch = self.dp.torch
         self.B = B
         dev = self.dp.device
@@ -364,14 +366,34 @@ def lambda_max_for(data, partition, penalty_kind="group", device=None):
 
 
 def regularization_path(data, loss, partition, n_lambdas=16, ratio=1e-3, penalty_kind="group", epochs=30,
-                        step="1/2L", seed=0, mode="async", device=None, keep_x=False, concurrent=1, batched=0):
+                        step="1/2L", seed=0, mode="async", device=None, keep_x=False, concurrent=1, batched=None):
     """Config 5 end to end on this rank's GPU (call under torchrun for N GPUs).
     ``batched`` = B > 0: the rank's lambdas B at a time through the
-    lambda-batched kernel; else ``concurrent`` lambdas at a time as forks."""
+    lambda-batched kernel; 0: ``concurrent`` lambdas at a time as forks (1 = one
+    after the other); None (default): the batched kernel with B = the rank's
+    share rounded up to a power of two (<= 16) where it applies (asynchronous
+    group lasso on contiguous blocks of <= 16, rows of <= 32 nonzeros), else
+    the forks."""
     lam_max = lambda_max_for(data, partition, penalty_kind, device=device)
     lams = lambda_grid(lam_max, n_lambdas, ratio)
-    solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
-                          keep_x=keep_x, concurrent=concurrent, batched=batched)
+    solve = None
+    if batched is None:
+        batched = 0
+        if penalty_kind == "group" and mode == "async" and concurrent == 1:
+            dist = _dist()
+            share = max(len(a) for a in assign(lams, dist.get_world_size() if dist else 1))
+            B = 1
+            while B < min(16, share):
+                B *= 2
+            try:
+                solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
+                                      keep_x=keep_x, batched=B)
+                batched = B
+            except ValueError:
+                solve = None
+    if solve is None:
+        solve = device_solver(data, loss, partition, penalty_kind, step, epochs, seed, mode, device=device,
+                              keep_x=keep_x, concurrent=concurrent, batched=batched)
     t0 = time.perf_counter()
     res = run_path(lams, solve)
     return {"lambda_max": lam_max, "lambdas": lams, "results": res, "seconds": time.perf_counter() - t0,

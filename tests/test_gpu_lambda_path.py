@@ -96,3 +96,21 @@ def test_concurrent_path_matches_serial_objectives(cuda, cfg5):
         tol = max(a["gap"], b["gap"]) + 1e-9 * abs(a["objective"])
         assert abs(a["objective"] - b["objective"]) <= tol, (a["lam"], a["objective"], a["gap"], b["objective"],
                                                              b["gap"])
+
+
+def test_regularization_path_defaults_to_the_batched_kernel(cuda, cfg5):
+    """regularization_path (the public config-5 driver) runs this rank's
+    lambdas through the lambda-batched kernel by default; its objectives agree
+    with the one-lambda-at-a-time group kernel schedule (batched=0) within each
+    other's certified gaps + 1e-6, and sparsity grows along the path."""
+    d, part, loss = cfg5["data"], cfg5["partition"], cfg5["loss"]
+    auto = lp.regularization_path(d, loss, part, n_lambdas=5, ratio=1e-2, epochs=150, seed=1)
+    serial = lp.regularization_path(d, loss, part, n_lambdas=5, ratio=1e-2, epochs=150, seed=1, batched=0)
+    assert auto["lambdas"] == serial["lambdas"] and len(auto["results"]) == 5
+    assert all(r["seconds"] == auto["results"][0]["seconds"] for r in auto["results"])  # one batched call
+    for a, b in zip(auto["results"], serial["results"]):
+        tol = 1e-6 * abs(b["objective"]) + max(a["gap"], 0.0) + max(b["gap"], 0.0)
+        assert abs(a["objective"] - b["objective"]) <= tol, (a["lam"], a["objective"], b["objective"])
+        assert a["gap"] >= -1e-12
+    nnz = [r["nnz"] for r in auto["results"]]
+    assert nnz[0] <= nnz[-1]
