@@ -931,7 +931,7 @@ def main():
                              f"lambda_max..1e-3 lambda_max, {args.path_epochs} async epochs each, "
                              "sharded over ranks (longest-work-first), matrix replicated",
                  "value": upd / (float(t[0].item()) / 1e3), "unit": UNIT, "max_rank_ms": float(t[0].item()),
-                 "schedule": f"lambda-batched kernel, B={lp_local['batched']} states per launch per rank, spread block layout",
+                 "schedule": f"lambda-batched kernel, B={lp_local['batched']} states per launch per rank, spread block order, the most frequent blocks scattered one coordinate sector per KB",
                  "concurrent_value": upd / (float(t[3].item()) / 1e3),
                  "concurrent_per_rank": lp_local["concurrent"], "rank0_ms_reps": lp_local["ms_reps"],
                  "rank0_certified_rel_gap_per_lambda_concurrent": lp_local["certified_rel_gap_concurrent"],
