@@ -251,9 +251,12 @@ int ps_batch_tune(int64_t rpad, int64_t rstride);
  * from B = 8 and 32 below (nhot = -1), 128 doubles = 1 KB; nhot = 0 or hstride = 0: every block in
  * the contiguous record).
  * hshare: a warp loads stored block 0 from L2 on every hshare-th of its rows and reads the CTA's
- * shared copy of it on the others (default 4; 0 = every row).
+ * shared copy of it on the others (default 4; 0 = every row).  hab: a hot slot keeps the states' x in
+ * one sector and their abar in another, hab doubles later (default -1: 64 = 512 B from B = 4, packed
+ * below; needs hstride >= hab + 2;
+ * 0 = one packed (x, abar) sector as everywhere else).
  * Process-wide; allocate states after setting */
-int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare);
+int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare, int32_t hab);
 /* the grid (CTAs, warps per CTA: rows in flight = their product) of this process's last ps_batch_run launch */
 int ps_batch_last_grid(int32_t *ctas, int32_t *warps_per_cta);
 /* field (0 x, 1 abar) of state beta <-> a p-vector (set = 0: state -> vec, 1: vec -> state);

@@ -120,7 +120,7 @@ def load():
         "ps_batch_run_rep": (_i32, [_P(Csr), _P(Part), _P(Params), _vp, _i32, _vp, _vp, _P(Sched), _vp, _i32, _i32, _vp]),
         "ps_batch_field": (_i32, [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp]),
         "ps_batch_tune": (_i32, [_i64, _i64]),
-        "ps_batch_tune2": (_i32, [_i32, _i64, _i32]),
+        "ps_batch_tune2": (_i32, [_i32, _i64, _i32, _i32]),
         "ps_batch_last_grid": (_i32, [_P(_i32), _P(_i32)]),
         "ps_batch_state_doubles": (_i64, [_i64, _i32, _i32]),
         "ps_batch_rep_doubles": (_i64, [_i32, _i32, _i32, _i32]),

@@ -34,6 +34,7 @@ namespace ps {
 struct BLay {
     int64_t body, region, hstride;  // doubles: nb*G*S*2; body + hot area + pad; per scattered coordinate
     int32_t G, S, hshift, nhot;
+    int32_t hab;  // hot slots: doubles from the x sector to the abar sector (0: one packed (x, abar) sector)
 };
 
 struct BArgs {
@@ -104,29 +105,44 @@ constexpr int BATCH_SM_SHARE = 32 * 8 * 2;     // per-CTA shared doubles: stored
 // 63.3, B = 4 43.5 -> 84.5, B = 2 78.8 -> 115 -- more than the replica
 // accumulators gave, which it replaces by default).  The pad (diagnostics)
 // shifts the regions against each other.
-__host__ __device__ __forceinline__ int64_t bidx(int64_t b, int q, int beta, const BLay &L)
+__host__ __device__ __forceinline__ int64_t bidx(int64_t b, int q, int beta, int field, const BLay &L)
 {
-    const int64_t base = (int64_t)(beta / L.S) * L.region + (beta % L.S) * 2;
+    const int slot = beta % L.S;
+    const int64_t base = (int64_t)(beta / L.S) * L.region;
     const int64_t r = b >> L.hshift;
-    if (r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0) return base + L.body + (r * L.G + q) * L.hstride;
-    return base + (b * L.G + q) * L.S * 2;
+    if (r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0) {
+        const int64_t hslot = base + L.body + (r * L.G + q) * L.hstride;
+        return L.hab ? hslot + slot + (int64_t)field * L.hab : hslot + slot * 2 + field;
+    }
+    return base + ((b * L.G + q) * L.S + slot) * 2 + field;
 }
 // the same address split for the kernel's block loops: coordinate q of stored
 // block b in this lane's state lives at lane_base + off + q * qs, with
 // lane_base = bidx(0, 0, beta) fixed per lane -- one hot test per block
 // instead of one per coordinate access
-__device__ __forceinline__ void bref(int64_t b, const BLay &L, int64_t &off, int &qs)
+// (hot slots with separate x / abar sectors: off carries the lane's -slot, the
+// abar of a coordinate sits da doubles after its x; da = 1 everywhere else)
+__device__ __forceinline__ void bref(int64_t b, int slot, const BLay &L, int64_t &off, int &qs, int &da)
 {
     const int64_t r = b >> L.hshift;
     const bool hot = r < L.nhot && (b & ((1ll << L.hshift) - 1)) == 0;
-    off = hot ? L.body + r * (L.G * L.hstride) : b * (L.G * L.S * 2);
+    off = hot ? L.body + r * (L.G * L.hstride) - (L.hab ? slot : 0) : b * (L.G * L.S * 2);
     qs = hot ? (int)L.hstride : L.S * 2;
+    da = hot && L.hab ? L.hab : 1;
+}
+// an (x, abar) pair: one 16-B load where they are adjacent
+__device__ __forceinline__ double2 ld_pair(const double *px, int da)
+{
+    if (da == 1) return ld_cg2(px);
+    return make_double2(ld_cg(px), ld_cg(px + da));
 }
 // layout knobs (doubles): the region pad and the stride of one (replica, hot
 // block) chunk of the replica accumulators; set by ps_batch_tune (diagnostics)
 static int64_t g_rpad = 0, g_rstride = 128;  // 1 KB replica chunks (tools/gpu/exp_batch_pad.py)
 static int64_t g_hstride = 128;  // scattered hot blocks: one sector per KB (adjacent lines measured slower below B = 16)
 static int32_t g_last_ctas = 0, g_last_wpc = 0;  // grid of the last ps_batch_run launch (ps_batch_last_grid)
+static int32_t g_hab = -1;       // hot slots: the abar sector this many doubles after the x sector (0: packed;
+                                 // -1: 64 = 512 B from B = 4, packed below: tools/gpu/exp_batch_scatter.py); ps_batch_tune2
 static int32_t g_hshare = 4;     // rows between a warp's own L2 loads of stored block 0 (0: every row); ps_batch_tune2
 static int32_t g_nhot = -1;      // how many: -1 = by B (128 from B = 8, else 32: tools/gpu/exp_batch_scatter.py); ps_batch_tune2
 
@@ -174,12 +190,12 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
     if (share) {
         if (wib == 0) {
             int64_t o0;
-            int q0;
-            bref(0, a.L, o0, q0);
+            int q0, d0;
+            bref(0, beta % S, a.L, o0, q0, d0);
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
-                hs[r] = q < G ? ld_cg2(st + o0 + q * q0)
+                hs[r] = q < G ? ld_pair(st + o0 + q * q0, d0)
                               : make_double2(0.0, 0.0);
             }
         }
@@ -212,12 +228,12 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         }
         // this lane's nonzero: the offset of x[col] from any lane's state base (one
         // layout lookup per nonzero; the margin loads and the abar REDs take it by shuffle)
-        int64_t eoff = 0;
+        int64_t eoff = 0;  // bit 0: a hot slot with separate x / abar sectors (the reader subtracts its slot)
         if (col >= 0) {
             const int be = col / G;
-            int eqs;
-            bref(be, a.L, eoff, eqs);
-            eoff += (col - be * G) * eqs;
+            int eqs, eda;
+            bref(be, 0, a.L, eoff, eqs, eda);
+            eoff += (col - be * G) * eqs + (eda != 1 ? 1 : 0);
         }
         const double yb = widen(__ldg(yp + i));
         double old = 0.0;  // alpha_i of this lane's state (lanes < B)
@@ -235,15 +251,15 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             if (lead == lane) sblk[rank] = blk;
         }
         __syncwarp();
-        auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs) {
+        auto load_blk = [&](int tb, double2 *v, int64_t &off, int &qs, int &da) {
             const int b = sblk[tb];
             const int nq = (int)min((int64_t)G, p - (int64_t)b * G);  // ragged last block
             const int rk = rep_rank<REP>(a, b);
-            bref(b, a.L, off, qs);
+            bref(b, beta % S, a.L, off, qs, da);
 #pragma unroll
             for (int r = 0; r < RMAX; r++) {
                 const int q = sub + LPB * r;
-                v[r] = q < nq ? ld_cg2(st + off + q * qs) : make_double2(0.0, 0.0);
+                v[r] = q < nq ? ld_pair(st + off + q * qs, da) : make_double2(0.0, 0.0);
                 if (rk >= 0 && q < nq)
                     for (int rr = 0; rr < a.nrep; rr++) v[r].x += ld_cg(rep_ptr(a, rr, rk, q, beta, B, G));
             }
@@ -254,12 +270,12 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         // (sps_step gathers x_hat once, saga.py:169-172)
         double2 bufa[RMAX], bufb[RMAX];
         int64_t aoff = 0, boff = 0;
-        int aqs = 0, bqs = 0;
+        int aqs = 0, bqs = 0, ada = 1, bda = 1;
         const bool hot0 = share && g > 0 && sblk[0] == 0;
         const bool fresh = !hot0 || (done + wib) % a.hshare == 0;
-        if (g > 0 && fresh) load_blk(0, bufa, aoff, aqs);
+        if (g > 0 && fresh) load_blk(0, bufa, aoff, aqs, ada);
         if (hot0 && !fresh) {
-            bref(0, a.L, aoff, aqs);
+            bref(0, beta % S, a.L, aoff, aqs, ada);
 #pragma unroll
             for (int r = 0; r < RMAX; r++) bufa[r] = hs[r];
         }
@@ -271,7 +287,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const int e = sub + LPB * j;
             const int64_t mo = __shfl_sync(FULL, eoff, e & 31);
             const bool need = e < k && !((first0 >> (e & 31)) & 1u);
-            xm[j] = need ? ld_cg(st + mo) : 0.0;
+            xm[j] = need ? ld_cg(st + (mo & ~1ll) - ((mo & 1) ? beta % S : 0)) : 0.0;
             if (REP) {
                 const int ce = __shfl_sync(FULL, col, e & 31);
                 const int rk = need ? rep_rank<REP>(a, ce / G) : -1;
@@ -315,7 +331,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
         // ---- every block of T_i, all B states; the next block's state loads
         // are issued before the current block is computed
         // two buffers in turn (no register copies between blocks)
-        auto process = [&](int tb, const double2 *cur, const int64_t coff, const int cqs) {
+        auto process = [&](int tb, const double2 *cur, const int64_t coff, const int cqs, const int cda) {
             const int b = sblk[tb];
             const double d = __shfl_sync(FULL, dB, tb);
             const double kd = a.kappa * d;
@@ -368,11 +384,11 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             }
         };
         for (int tb = 0; tb < g; tb += 2) {  // block 0 is in bufa already
-            if (tb + 1 < g) load_blk(tb + 1, bufb, boff, bqs);
-            process(tb, bufa, aoff, aqs);
+            if (tb + 1 < g) load_blk(tb + 1, bufb, boff, bqs, bda);
+            process(tb, bufa, aoff, aqs, ada);
             if (tb + 1 < g) {
-                if (tb + 2 < g) load_blk(tb + 2, bufa, aoff, aqs);
-                process(tb + 1, bufb, boff, bqs);
+                if (tb + 2 < g) load_blk(tb + 2, bufa, aoff, aqs, ada);
+                process(tb + 1, bufb, boff, bqs, bda);
             }
         }
         // ---- abar on S_i: ((new - replaced)/n) a_i
@@ -383,7 +399,7 @@ __global__ void BATCH_BOUNDS sps_group_batch_kernel(const BArgs a)
             const int64_t ao = __shfl_sync(FULL, eoff, e & 31);
             const double ve = __shfl_sync(FULL, val, e & 31);
             if (e < k) {
-                double *pab = st + ao + 1;
+                double *pab = (ao & 1) ? st + (ao & ~1ll) - beta % S + a.L.hab : st + ao + 1;
                 if (a.det) *pab = *pab + tq * ve;
                 else red_add(pab, tq * ve);
             }
@@ -422,7 +438,7 @@ __global__ void k_batch_field(const double *state, int64_t p, const BLay L, int 
 {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = j / L.G;
-        double *s = const_cast<double *>(state) + bidx(b, (int)(j - b * L.G), beta, L) + field;
+        double *s = const_cast<double *>(state) + bidx(b, (int)(j - b * L.G), beta, field, L);
         if (set) *s = out[j];
         else out[j] = *s;
     }
@@ -445,7 +461,7 @@ __global__ void k_batch_fold(double *state, double *xrep, int nrep, int nrb, int
             *r = 0.0;
         }
         const int64_t b = (int64_t)rank << hshift;
-        if (b * G + q < p) state[bidx(b, q, beta, L)] += sum;
+        if (b * G + q < p) state[bidx(b, q, beta, 0, L)] += sum;
     }
 }
 
@@ -459,9 +475,11 @@ static BLay batch_layout(int64_t p, int G, int B, int hshift)
     L.G = G;
     L.S = B < BATCH_S ? B : BATCH_S;
     L.body = ((p + G - 1) / G) * G * L.S * 2;
-    L.hstride = std::max<int64_t>(g_hstride, 2 * L.S);
+    L.hstride = (std::max<int64_t>(g_hstride, 2 * L.S) + 1) & ~1ll;  // even: bit 0 of a shuffled offset is a flag
     L.nhot = g_hstride > 0 ? (g_nhot >= 0 ? g_nhot : (B >= 8 ? 128 : 32)) : 0;
     L.hshift = std::max(0, std::min(hshift, 30));
+    const int hab = g_hab >= 0 ? g_hab : (B >= 4 ? 64 : 0);
+    L.hab = (hab > 0 && L.hstride >= hab + L.S) ? hab : 0;
     L.region = L.body + (int64_t)L.nhot * G * L.hstride + g_rpad;
     return L;
 }
@@ -587,9 +605,10 @@ extern "C" int ps_batch_last_grid(int32_t *ctas, int32_t *warps_per_cta)
     return PS_OK;
 }
 
-extern "C" int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare)
+extern "C" int ps_batch_tune2(int32_t nhot, int64_t hstride, int32_t hshare, int32_t hab)
 {
-    if (nhot < -1 || hstride < 0 || hshare < 0) return ps_fail(PS_EINVAL, "bad argument");
+    if (nhot < -1 || hstride < 0 || hshare < 0 || hab < -1) return ps_fail(PS_EINVAL, "bad argument");
+    g_hab = hab;
     g_nhot = nhot;
     g_hstride = hstride;
     g_hshare = hshare;

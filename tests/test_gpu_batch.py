@@ -56,24 +56,26 @@ def tune2():
     """ps_batch_tune2 with the defaults restored afterwards."""
     from paper_1707_06468_b200 import _lib
 
-    def set_(nhot, hstride, hshare):
-        _lib.check(_lib.load().ps_batch_tune2(nhot, hstride, hshare))
+    def set_(nhot, hstride, hshare, hab):
+        _lib.check(_lib.load().ps_batch_tune2(nhot, hstride, hshare, hab))
 
     yield set_
-    set_(-1, 128, 4)
+    set_(-1, 128, 4, -1)
 
 
 @pytest.mark.parametrize("B,factors,nrep,layout", [
     (8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005), 0, None), (2, (0.3, 0.01), 0, None), (16, (0.5, 0.01), 0, None),
     (8, (0.5, 0.2, 0.1, 0.05, 0.03, 0.02, 0.01, 0.005), 4, None), (2, (0.3, 0.01), 8, None),
-    (4, (0.5, 0.1, 0.03, 0.01), 0, (-1, 128, 0)), (4, (0.5, 0.1, 0.03, 0.01), 0, (0, 0, 0))],
-    ids=["B8", "B2", "B16", "B8rep", "B2rep", "B4noshare", "B4contiguous"])
+    (4, (0.5, 0.1, 0.03, 0.01), 0, (-1, 128, 0, 64)), (4, (0.5, 0.1, 0.03, 0.01), 0, (0, 0, 0, 0)),
+    (4, (0.5, 0.1, 0.03, 0.01), 0, (-1, 128, 4, 0))],
+    ids=["B8", "B2", "B16", "B8rep", "B2rep", "B4noshare", "B4contiguous", "B4packed"])
 def test_batched_async_reaches_each_optimum(cuda, tune2, B, factors, nrep, layout):
     """Spread block layout with the scattered hot blocks of the state (the
     default: no replicas), and the opt-in replicated x-delta accumulators of the
     hottest blocks (ps_batch_run_rep, folded after the launch).  Layout variants
     (ps_batch_tune2): every row loading stored block 0 itself (no CTA-shared
-    copy), and every block in the contiguous record (no scattered hot blocks)."""
+    copy), every block in the contiguous record (no scattered hot blocks), and
+    hot slots with one packed (x, abar) sector."""
     if layout is not None:
         tune2(*layout)
     rng = np.random.default_rng(11)

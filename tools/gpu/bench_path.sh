@@ -1,5 +1,5 @@
 # the bench line restricted to config 2 and the lambda path (config 5), with the per-lambda summary printed
-python bench.py --no-cpu --no-big --no-io --no-extra --detail-out gpurun_out/bench_detail_sc6.json > gpurun_out/bench_path.json 2> gpurun_out/bench_path.err
+python bench.py --no-cpu --no-big --no-io --no-extra --detail-out gpurun_out/bench_detail_path.json > gpurun_out/bench_path.json 2> gpurun_out/bench_path.err
 tail -3 gpurun_out/bench_path.err
 python - <<'PY'
 import json

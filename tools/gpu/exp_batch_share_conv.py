@@ -27,7 +27,7 @@ for lam in lams[-3:]:
     frefs.append(dp.objective())
 VARIANTS = [(0, 0, 0), (-1, 128, 0), (-1, 128, 4)] * 2 if len(sys.argv) < 2 else [tuple(int(t) for t in v.split(":")) for v in sys.argv[1].split(",")]
 for nhot, hstride, hs in VARIANTS:
-    _lib.check(_lib.load().ps_batch_tune2(nhot, hstride, hs))
+    _lib.check(_lib.load().ps_batch_tune2(nhot, hstride, hs, -1))
     for seed in (3, 4, 5):
         bp = BatchedPath(data, loss, part, B=8)
         gamma = resolve_step_size("1/2L", bp.dp.L, n, lam1)
