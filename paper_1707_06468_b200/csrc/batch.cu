@@ -11,8 +11,8 @@
 //
 // State layout (bidx below): states in groups of 2, each group its own
 // region [block][q][2](x, abar) followed by a hot area where the most frequent
-// blocks keep one coordinate sector per KB (the L2 serialises the atomics of a
-// 128-B line); alpha[i*B + beta]; the block weights d_B come from ps_prepare
+// blocks keep one coordinate per KB, x and abar in separate sectors (the L2
+// serialises the atomics of a 128-B line); alpha[i*B + beta]; the block weights d_B come from ps_prepare
 // (part->blk_weight).  The first block of T_i is loaded once per row (margin
 // and prox share it), stored block 0 at most every hshare-th row per warp.
 //
